@@ -1,0 +1,48 @@
+"""Shared test helpers: run the oracle on a workloads.Problem in a given layout,
+and the per-element acceptance check of BASELINE.json's north_star."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+import workloads
+
+
+def stored(prob: workloads.Problem, layouts: str, lda=None, ldb=None):
+    """Storage tensors (CPU fp16) and leading dims of A and B for layout pair e.g. 'rc'."""
+    As, lda = workloads.store(prob.A, layouts[0], lda)
+    Bs, ldb = workloads.store(prob.B, layouts[1], ldb)
+    return As, lda, Bs, ldb
+
+
+def oracle_run(prob: workloads.Problem, layouts: str = "rr", *, relu=True, bias_mode=None, rows=None,
+               cols=None, literal_round=False, lda=None, ldb=None, nthreads=None):
+    bias_mode = prob.meta.get("bias_mode") if bias_mode is None else bias_mode
+    As, lda, Bs, ldb = stored(prob, layouts, lda, ldb)
+    ldbias = prob.bias.shape[1] if (prob.bias is not None and prob.bias.dim() == 2) else 0
+    return oracle.gemm_epilogue(
+        As, Bs, prob.M, prob.N, prob.K,
+        layoutA="row" if layouts[0] == "r" else "col", layoutB="row" if layouts[1] == "r" else "col",
+        lda=lda, ldb=ldb, bias=prob.bias, bias_mode=bias_mode if prob.bias is not None else None,
+        ldbias=ldbias, relu=relu, prologue=prob.meta.get("prologue"), scale=prob.scale,
+        literal_round=literal_round, rows=rows, cols=cols, nthreads=nthreads)
+
+
+def check_bound(got: np.ndarray, out: np.ndarray, mag: np.ndarray, what: str = ""):
+    """|got - out| <= 4e-3*mag + 1e-3*|out| element-wise (BASELINE.json north_star).
+    A 2^-25 absolute slack covers fp16 subnormal outputs with tiny mag (DESIGN.md R-TOL)."""
+    got = np.asarray(got, dtype=np.float64)
+    tol = oracle.bound(out, mag) + 2.0 ** -25
+    err = np.abs(got - out)
+    bad = ~(err <= tol)
+    if bad.any():
+        idx = np.argwhere(bad)[:5]
+        msg = "; ".join(f"{tuple(i)} got={got[tuple(i)]!r} want={out[tuple(i)]!r} tol={tol[tuple(i)]:.3g}"
+                        for i in idx)
+        raise AssertionError(f"{what}: {int(bad.sum())} / {bad.size} elements outside the bound: {msg}")
+    return float(np.max(err / np.maximum(tol, 1e-300))) if err.size else 0.0
+
+
+def f16_bits(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
