@@ -1,0 +1,182 @@
+/*
+ * gemm_epilogue.h -- C ABI of the B200 (sm_100a) fused fp16 GEMM + bias + ReLU library.
+ *
+ * The operation is the epilogue-fusion idiom of "Automatic Kernel Generation for
+ * Volta Tensor Cores" (arXiv 2006.12645), Listing 1:
+ *
+ *     S1: C[i,j] = sum_k A[i,k] * B[k,j]            fp16 inputs, fp32 accumulation
+ *     S2: E[i,j] = relu_add(C[i,j], bias[.])         ReLU at the root
+ *
+ * computed in ONE kernel with no global write of the intermediate C
+ * (Sec. VII-A "Avoiding Intermediate Writes To Global Memory"),
+ * optionally with a pointwise prologue on A (Sec. VII-C, Listing 5).
+ * Readings of the paper that this interface fixes are listed in DESIGN.md (R-C1..R-C16).
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ * Element addressing (leading dimension ld counted in ELEMENTS; 0 = packed):
+ *     A row-major: a(i,k) = A[i*lda + k], lda >= K      A col-major: a(i,k) = A[k*lda + i], lda >= M
+ *     B row-major: b(k,j) = B[k*ldb + j], ldb >= N      B col-major: b(k,j) = B[j*ldb + k], ldb >= K
+ *     C is always row-major: c(i,j) = C[i*ldc + j], ldc >= N (PAPER.md:869 stores row-major)
+ * Layout pair names: rr, rc, cr, cc = (layout of A, layout of B).  rc is the paper's Listing 2
+ * case (A row x B col).  In PyTorch terms rr is `A @ B`.
+ * Types: A, B, bias are IEEE binary16; prologue_scale is fp32; C is fp16 (the paper's,
+ * PAPER.md:844, 896-897) or fp32 (GE_OUT_F32).  Accumulation is fp32 in Tensor Memory.
+ * Epilogue arithmetic is fp32 (acc + bias, then ReLU y = v > 0 ? v : +0), rounded once
+ * with round-to-nearest-even at the store (DESIGN.md R-C3, R-C5, R-C6).
+ * Ownership: the caller owns every buffer.  The library never allocates device memory on
+ * the device-pointer entry points and never retains a pointer after the call returns
+ * (the kernel may still be reading it until the stream reaches that point).
+ * Streams: device-pointer entry points are asynchronous on `stream` (a cudaStream_t,
+ * NULL = legacy default stream) and never synchronize the device.  Results are valid
+ * once the caller synchronizes the stream.  Calls are thread-safe.
+ * Errors: argument errors are returned synchronously BEFORE any launch, with nothing
+ * written.  GE_ERR_CUDA reports a launch failure (detail: ge_last_error_detail()).
+ * Asynchronous device faults surface at the caller's next synchronization.
+ * Alignment (Tensor Memory Accelerator rules): A and B base pointers must be 16-byte
+ * aligned and lda*2, ldb*2 (and batch strides *2) multiples of 16 bytes, else
+ * GE_ERR_MISALIGNED.  C, bias and scale have no alignment requirement: a C whose base or
+ * ldc is not 16-byte compatible is written by a st.global epilogue instead of TMA stores.
+ * Aliasing: C must not overlap A, B, bias or scale (`__restrict__`), else
+ * GE_ERR_ALIASING.
+ * Degenerate sizes: M == 0 or N == 0 (or batch == 0) is a no-op returning GE_OK.
+ * K == 0 gives C = op(bias) (DESIGN.md R-C9).
+ */
+#ifndef GEMM_EPILOGUE_H
+#define GEMM_EPILOGUE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { GE_ROW_MAJOR = 0, GE_COL_MAJOR = 1 } ge_layout;
+
+typedef enum { GE_OUT_F16 = 0, GE_OUT_F32 = 1 } ge_out_dtype;
+
+/* The pointwise epilogue (S2 of Listing 1).  BIAS needs a non-NULL bias pointer. */
+typedef enum {
+    GE_EPI_NONE = 0,        /* C = A.B                         (Listing 2, plain GEMM)       */
+    GE_EPI_BIAS = 1,        /* C = A.B + beta                                               */
+    GE_EPI_RELU = 2,        /* C = relu(A.B)                                                 */
+    GE_EPI_BIAS_RELU = 3    /* C = relu(A.B + beta)            (Listing 1, relu_add)         */
+} ge_epilogue_op;
+
+/* Shape of the bias operand beta (DESIGN.md R-C2). */
+typedef enum {
+    GE_BIAS_ROW = 0,        /* beta(i,j) = bias[j], length N (default; the DL idiom)          */
+    GE_BIAS_COL = 1,        /* beta(i,j) = bias[i], length M                                  */
+    GE_BIAS_FULL = 2        /* beta(i,j) = bias[i*ldbias + j], M x N (paper-literal) */
+} ge_bias_mode;
+
+/* Pointwise prologue applied to A before the contraction (Sec. VII-C, DESIGN.md R-C12). */
+typedef enum {
+    GE_PRO_NONE = 0,
+    GE_PRO_SCALE_K = 1,     /* a'(i,k) = fp16_rne(s[k] * a(i,k)), s = prologue_scale, fp32, length K */
+    GE_PRO_RELU = 2         /* a'(i,k) = max(a(i,k), +0)  (Listing 5)          */
+} ge_prologue_op;
+
+typedef struct {
+    int32_t bias_mode;              /* ge_bias_mode */
+    int64_t ldbias;                 /* FULL only: row stride of bias in elements (0 = N) */
+    int32_t prologue;               /* ge_prologue_op */
+    const float* prologue_scale;    /* SCALE_K only: device pointer (host pointer for *_host), length K */
+    int32_t out_dtype;              /* ge_out_dtype */
+    int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128 or 256) */
+    int32_t cta_group;              /* 0 = heuristic; 1 = single-CTA tiles; 2 = CTA-pair tiles */
+} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0} */
+
+typedef enum {
+    GE_OK = 0,
+    GE_ERR_INVALID_VALUE = 1,       /* negative size, ld too small, NULL pointer that is needed, bad enum */
+    GE_ERR_MISALIGNED = 2,          /* A/B base or stride breaks the 16-byte TMA rules */
+    GE_ERR_ALIASING = 3,            /* C overlaps an input */
+    GE_ERR_UNSUPPORTED_DEVICE = 4,  /* current device is not sm_100 or no device */
+    GE_ERR_CUDA = 5                 /* a CUDA runtime/driver call failed */
+} ge_status;
+
+/*
+ * Single GEMM: C = epilogue(prologue(A) . B).  All pointers are device pointers on the
+ * current device; `stream` is a cudaStream_t.  See conventions above.
+ */
+ge_status gemm_epilogue(int64_t M, int64_t N, int64_t K,
+                        int32_t layoutA, int32_t layoutB,
+                        const void* A, int64_t lda,
+                        const void* B, int64_t ldb,
+                        const void* bias,
+                        void* C, int64_t ldc,
+                        int32_t op, const ge_options* opt, void* stream);
+
+/*
+ * Strided-batched GEMM (DESIGN.md R-C14): item b uses A + b*strideA, B + b*strideB,
+ * C + b*strideC and bias + b*strideBias (strides in ELEMENTS; strideBias = 0 shares one
+ * bias).  All items share M, N, K, layouts and options.  One persistent launch covers the
+ * whole batch (the batch index is the slowest coordinate of the tile id).
+ */
+ge_status gemm_epilogue_batched(int64_t batch, int64_t M, int64_t N, int64_t K,
+                                int32_t layoutA, int32_t layoutB,
+                                const void* A, int64_t lda, int64_t strideA,
+                                const void* B, int64_t ldb, int64_t strideB,
+                                const void* bias, int64_t strideBias,
+                                void* C, int64_t ldc, int64_t strideC,
+                                int32_t op, const ge_options* opt, void* stream);
+
+/*
+ * Host-buffer variant (end-to-end path): same arguments as gemm_epilogue_batched but
+ * A, B, bias, prologue_scale and C are HOST pointers (pinned memory gives full PCIe
+ * bandwidth; pageable works).  The call copies the inputs to a library-owned device
+ * workspace on `stream`, runs the fused kernel, copies C back and synchronizes `stream`
+ * before returning.  The workspace grows on demand, is kept per device for reuse and is
+ * released by ge_release_workspace().  Operand alignment rules apply to ld/strides only.
+ */
+ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K,
+                             int32_t layoutA, int32_t layoutB,
+                             const void* A, int64_t lda, int64_t strideA,
+                             const void* B, int64_t ldb, int64_t strideB,
+                             const void* bias, int64_t strideBias,
+                             void* C, int64_t ldc, int64_t strideC,
+                             int32_t op, const ge_options* opt, void* stream);
+
+/* Frees the workspace of gemm_epilogue_host on the current device. */
+ge_status ge_release_workspace(void);
+
+/*
+ * Argument validation only (no device access, no launch): returns what the batched entry
+ * point would return for these arguments before touching the GPU.  Pointers are only
+ * compared and alignment-checked, never dereferenced.
+ */
+ge_status ge_validate(int64_t batch, int64_t M, int64_t N, int64_t K,
+                      int32_t layoutA, int32_t layoutB,
+                      const void* A, int64_t lda, int64_t strideA,
+                      const void* B, int64_t ldb, int64_t strideB,
+                      const void* bias, int64_t strideBias,
+                      void* C, int64_t ldc, int64_t strideC,
+                      int32_t op, const ge_options* opt);
+
+/* Static, never-NULL description of a status code. */
+const char* ge_status_string(ge_status status);
+
+/* Thread-local detail of the last non-OK status on this thread ("" if none). */
+const char* ge_last_error_detail(void);
+
+/*
+ * Describes the configuration the heuristic picks for a shape (no device access):
+ * writes tile_m, tile_n, cta_group, stages and the number of output tiles.
+ */
+ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
+                  const ge_options* opt, int32_t num_sms,
+                  int32_t* tile_m, int32_t* tile_n, int32_t* cta_group, int32_t* stages,
+                  int64_t* num_tiles);
+
+/* Number of fused kernels this library has launched in this process (for launch accounting). */
+uint64_t ge_launch_count(void);
+
+/* Library version string. */
+const char* ge_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEMM_EPILOGUE_H */

@@ -1,0 +1,268 @@
+"""paper_2006_12645_b200 -- fused fp16 GEMM + bias + ReLU for B200 (sm_100a).
+
+Thin Python binding over the C ABI in ``include/gemm_epilogue.h`` (library
+``libgemm_epilogue.so`` built in-tree by ``_build.py``).  This module only marshals
+arguments (torch tensors -> pointers, strides -> leading dimensions, the current CUDA
+stream); every step of the computation runs in the CUDA kernels.  There is no CPU
+fallback: if the shared library is missing or the device is not sm_100 the calls raise.
+
+Operation (Listing 1; prologue: Listing 5):
+    C = epilogue(prologue(A) @ B),  epilogue = relu_add(., bias) by default.
+
+Operands are LOGICAL matrices: ``A`` is M x K and ``B`` is K x N (optionally with a leading
+batch dimension).  Each may be row-major (stride(-1) == 1) or column-major (stride(-2) == 1,
+e.g. ``X.t()``); the layout pair is detected from the strides (rr, rc, cr, cc).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+__all__ = ["gemm_epilogue", "gemm_epilogue_batched", "gemm_epilogue_host", "GEError", "plan", "validate_args",
+           "launch_count", "version", "library_path", "load_library", "layout_of", "Status"]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libgemm_epilogue.so")
+_lib = None
+
+
+class Status:
+    OK = 0
+    INVALID_VALUE = 1
+    MISALIGNED = 2
+    ALIASING = 3
+    UNSUPPORTED_DEVICE = 4
+    CUDA = 5
+
+
+EPI = {"none": 0, "bias": 1, "relu": 2, "bias_relu": 3}
+BIAS_MODE = {"row": 0, "col": 1, "full": 2}
+PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
+
+
+class GEOptions(ctypes.Structure):
+    _fields_ = [("bias_mode", ctypes.c_int32), ("ldbias", ctypes.c_int64), ("prologue", ctypes.c_int32),
+                ("prologue_scale", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("tile_n", ctypes.c_int32),
+                ("cta_group", ctypes.c_int32)]
+
+
+class GEError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        super().__init__(f"{_lib.ge_status_string(status).decode()} ({detail})" if _lib else f"status {status}")
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libgemm_epilogue.so (built by __graft_entry__.build() / _build.py).  Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    I64, I32, P = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    OPT = ctypes.POINTER(GEOptions)
+    lib.gemm_epilogue.restype = I32
+    lib.gemm_epilogue.argtypes = [I64, I64, I64, I32, I32, P, I64, P, I64, P, P, I64, I32, OPT, P]
+    batched = [I64, I64, I64, I64, I32, I32, P, I64, I64, P, I64, I64, P, I64, P, I64, I64, I32, OPT]
+    lib.gemm_epilogue_batched.restype = I32
+    lib.gemm_epilogue_batched.argtypes = batched + [P]
+    lib.gemm_epilogue_host.restype = I32
+    lib.gemm_epilogue_host.argtypes = batched + [P]
+    lib.ge_validate.restype = I32
+    lib.ge_validate.argtypes = batched
+    lib.ge_release_workspace.restype = I32
+    lib.ge_release_workspace.argtypes = []
+    lib.ge_status_string.restype = ctypes.c_char_p
+    lib.ge_status_string.argtypes = [I32]
+    lib.ge_last_error_detail.restype = ctypes.c_char_p
+    lib.ge_last_error_detail.argtypes = []
+    lib.ge_plan.restype = I32
+    lib.ge_plan.argtypes = [I64, I64, I64, I64, I32, I32, OPT, I32, ctypes.POINTER(I32), ctypes.POINTER(I32),
+                            ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64)]
+    lib.ge_launch_count.restype = ctypes.c_uint64
+    lib.ge_launch_count.argtypes = []
+    lib.ge_version.restype = ctypes.c_char_p
+    lib.ge_version.argtypes = []
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != Status.OK:
+        raise GEError(status, _lib.ge_last_error_detail().decode())
+
+
+def layout_of(x: torch.Tensor):
+    """(layout, ld) of the last two dims of a logical matrix view: 0 = row-major, 1 = col-major."""
+    R, C = x.shape[-2], x.shape[-1]
+    s0, s1 = x.stride(-2), x.stride(-1)
+    up8 = lambda v: (max(v, 1) + 7) // 8 * 8     # a single row/column: any ld >= extent is valid
+    if C == 1 and s0 == 1 and R > 1:
+        return 1, up8(R)
+    if (s1 == 1 or C <= 1) and (R <= 1 or s0 >= C):
+        return 0, (s0 if R > 1 else up8(C))
+    if (s0 == 1 or R <= 1) and (C <= 1 or s1 >= R):
+        return 1, (s1 if C > 1 else up8(R))
+    raise ValueError(f"operand with shape {tuple(x.shape)} and strides {x.stride()} is neither row- nor column-major")
+
+
+def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group):
+    o = GEOptions()
+    o.bias_mode = BIAS_MODE[bias_mode]
+    o.ldbias = int(ldbias or 0)
+    o.prologue = PROLOGUE[prologue]
+    o.prologue_scale = scale.data_ptr() if scale is not None else None
+    o.out_dtype = 1 if out_dtype == torch.float32 else 0
+    o.tile_n = int(tile_n)
+    o.cta_group = int(cta_group)
+    return o
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _op(op: str, bias) -> int:
+    if op is None:
+        op = "bias_relu" if bias is not None else "relu"
+    return EPI[op]
+
+
+def _bias_ld(bias, bias_mode):
+    if bias is None:
+        return 0, 0
+    if bias_mode == "full":
+        if bias.stride(-1) != 1:
+            raise ValueError("FULL bias must be row-major (stride(-1) == 1)")
+        return bias.stride(-2), (bias.stride(0) if bias.dim() == 3 else 0)
+    if bias.stride(-1) != 1:
+        raise ValueError("bias vector must be contiguous")
+    return 0, (bias.stride(0) if bias.dim() == 2 else 0)
+
+
+def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None, *, op: Optional[str] = None,
+                  bias_mode: str = "row", prologue: Optional[str] = None, scale: Optional[torch.Tensor] = None,
+                  out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
+                  cta_group: int = 0, stream=None) -> torch.Tensor:
+    """C = relu_add(prologue(A) @ B, bias) on the current CUDA device (fp16 in, fp32 accumulate).
+
+    A: (M, K) fp16, B: (K, N) fp16, row- or column-major views.  bias: (N,) for bias_mode "row",
+    (M,) for "col", (M, ldbias>=N) row-major for "full".  op in {"none","bias","relu","bias_relu"}
+    (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32) or "relu".
+    Returns C (M, N) row-major in out_dtype (fp16 or fp32), asynchronously on the current stream.
+    """
+    lib = load_library()
+    if A.dim() != 2 or B.dim() != 2:
+        raise ValueError("use gemm_epilogue_batched for 3-D operands")
+    M, K = A.shape
+    K2, N = B.shape
+    if K2 != K:
+        raise ValueError(f"inner dimensions differ: A is {tuple(A.shape)}, B is {tuple(B.shape)}")
+    la, lda = layout_of(A)
+    lb, ldb = layout_of(B)
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=A.device)
+    if out.stride(-1) != 1 and N > 1:
+        raise ValueError("out must be row-major")
+    ldbias, _ = _bias_ld(bias, bias_mode)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group)
+    st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
+                           bias.data_ptr() if bias is not None else None, out.data_ptr(), max(out.stride(0), N, 1),
+                           _op(op, bias), ctypes.byref(o), _stream(stream))
+    _check(st)
+    return out
+
+
+def _batched_args(A, B, bias, bias_mode, out):
+    if A.dim() != 3 or B.dim() != 3:
+        raise ValueError("batched operands are (batch, rows, cols)")
+    batch, M, K = A.shape
+    _, K2, N = B.shape
+    if K2 != K or B.shape[0] != batch:
+        raise ValueError("batched shapes disagree")
+    la, lda = layout_of(A)
+    lb, ldb = layout_of(B)
+    ldbias, sbias = _bias_ld(bias, bias_mode)
+    return batch, M, N, K, la, lda, A.stride(0), lb, ldb, B.stride(0), ldbias, sbias
+
+
+def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None, *,
+                          op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
+                          scale: Optional[torch.Tensor] = None, out_dtype: torch.dtype = torch.float16,
+                          out: Optional[torch.Tensor] = None, tile_n: int = 0, cta_group: int = 0,
+                          stream=None) -> torch.Tensor:
+    """Strided-batched form: A (b, M, K), B (b, K, N), bias (N,)/(b, N) [row], (M,)/(b, M) [col],
+    (M, ld)/(b, M, ld) [full]; a 1-D/2-D bias is shared by every item.  One persistent launch."""
+    lib = load_library()
+    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A, B, bias, bias_mode, out)
+    if out is None:
+        out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group)
+    st = lib.gemm_epilogue_batched(batch, M, N, K, la, lb, A.data_ptr(), lda, sA, B.data_ptr(), ldb, sB,
+                                   bias.data_ptr() if bias is not None else None, sbias, out.data_ptr(),
+                                   max(out.stride(1), N, 1), out.stride(0), _op(op, bias), ctypes.byref(o),
+                                   _stream(stream))
+    _check(st)
+    return out
+
+
+def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None, *,
+                       op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
+                       scale: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                       out_dtype: torch.dtype = torch.float16, tile_n: int = 0, cta_group: int = 0,
+                       stream=None) -> torch.Tensor:
+    """End-to-end path through the C ABI with HOST (CPU, ideally pinned) tensors: the library copies
+    the inputs to the device, runs the fused kernel and copies C back, synchronously."""
+    lib = load_library()
+    A3 = A if A.dim() == 3 else A.unsqueeze(0)
+    B3 = B if B.dim() == 3 else B.unsqueeze(0)
+    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A3, B3, bias, bias_mode, out)
+    if out is None:
+        out = torch.empty((batch, M, N) if A.dim() == 3 else (M, N), dtype=out_dtype,
+                          pin_memory=A.is_pinned())
+    out3 = out if out.dim() == 3 else out.unsqueeze(0)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group)
+    st = lib.gemm_epilogue_host(batch, M, N, K, la, lb, A3.data_ptr(), lda, sA, B3.data_ptr(), ldb, sB,
+                                bias.data_ptr() if bias is not None else None, sbias, out3.data_ptr(),
+                                max(out3.stride(1), N, 1), out3.stride(0), _op(op, bias), ctypes.byref(o),
+                                _stream(stream))
+    _check(st)
+    return out
+
+
+def validate_args(*args) -> int:
+    """Raw ge_validate (19 arguments, see include/gemm_epilogue.h); returns the status code."""
+    return load_library().ge_validate(*args)
+
+
+def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: int = 148, tile_n: int = 0,
+         cta_group: int = 0) -> dict:
+    lib = load_library()
+    o = _options("row", 0, None, None, torch.float16, tile_n, cta_group)
+    tm, tn, cg, stg = (ctypes.c_int32() for _ in range(4))
+    nt = ctypes.c_int64()
+    st = lib.ge_plan(batch, M, N, K, 0 if layouts[0] == "r" else 1, 0 if layouts[1] == "r" else 1, ctypes.byref(o),
+                     num_sms, ctypes.byref(tm), ctypes.byref(tn), ctypes.byref(cg), ctypes.byref(stg),
+                     ctypes.byref(nt))
+    _check(st)
+    return {"tile_m": tm.value, "tile_n": tn.value, "cta_group": cg.value, "stages": stg.value,
+            "num_tiles": nt.value}
+
+
+def launch_count() -> int:
+    return int(load_library().ge_launch_count())
+
+
+def version() -> str:
+    return load_library().ge_version().decode()

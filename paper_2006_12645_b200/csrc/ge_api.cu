@@ -1,0 +1,503 @@
+// ge_api.cu -- host runtime behind include/gemm_epilogue.h: argument validation, the tile
+// configuration heuristic, TMA tensor-map encoding, persistent grid sizing and the launch.
+//
+// Launch inference in the paper comes from schedule constraints (one
+// 128x128 block per output tile, grid (N/128, M/128)).  Here the grid is
+// persistent: min(#tiles, #SMs) CTAs (CTA pairs for cta_group 2) walk the tile sequence.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gemm_epilogue.h"
+#include "ge_launch.cuh"
+
+namespace {
+
+thread_local std::string g_detail;
+std::atomic<uint64_t> g_launches{0};
+
+ge_status fail(ge_status s, const std::string& why) {
+    g_detail = why;
+    return s;
+}
+
+constexpr int64_t kMaxDim = (1ll << 31) - 1;
+
+struct Dev {
+    bool probed = false;
+    bool ok = false;
+    int sms = 0;
+};
+std::mutex g_dev_mu;
+Dev g_devs[64];
+
+ge_status device_info(int* sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return fail(GE_ERR_UNSUPPORTED_DEVICE, "no CUDA device");
+    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    Dev& d = g_devs[dev];
+    if (!d.probed) {
+        int major = 0, minor = 0, n = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cudaGetLastError();
+        d.ok = (major == 10 && minor == 0);
+        d.sms = n;
+        d.probed = true;
+    }
+    if (!d.ok) return fail(GE_ERR_UNSUPPORTED_DEVICE, "device is not sm_100 (B200); this library targets sm_100a");
+    *sms = d.sms;
+    return GE_OK;
+}
+
+// ------------------------------------------------------------------ validation
+struct Args {
+    int64_t batch, M, N, K;
+    int32_t la, lb;
+    const void* A;
+    int64_t lda, sA;
+    const void* B;
+    int64_t ldb, sB;
+    const void* bias;
+    int64_t sBias;
+    void* C;
+    int64_t ldc, sC;
+    int32_t op;
+    ge_options o;
+};
+
+int64_t extent_bytes(int64_t batch, int64_t outer, int64_t inner, int64_t ld, int64_t stride, int es) {
+    if (batch == 0 || outer == 0 || inner == 0) return 0;
+    return ((batch - 1) * stride + (outer - 1) * ld + inner) * es;
+}
+
+bool overlap(const void* a, int64_t na, const void* b, int64_t nb) {
+    if (!a || !b || na <= 0 || nb <= 0) return false;
+    const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + static_cast<uintptr_t>(nb) && y < x + static_cast<uintptr_t>(na);
+}
+
+bool has_bias(int32_t op) { return op == GE_EPI_BIAS || op == GE_EPI_BIAS_RELU; }
+bool has_relu(int32_t op) { return op == GE_EPI_RELU || op == GE_EPI_BIAS_RELU; }
+
+// Normalises ld/stride defaults in place and checks everything that can be checked on the host.
+ge_status validate(Args& a) {
+    char buf[256];
+    if (a.batch < 0 || a.M < 0 || a.N < 0 || a.K < 0)
+        return fail(GE_ERR_INVALID_VALUE, "negative size");
+    if (a.M > kMaxDim || a.N > kMaxDim || a.K > kMaxDim || a.batch > kMaxDim)
+        return fail(GE_ERR_INVALID_VALUE, "size exceeds 2^31-1");
+    if ((a.la != GE_ROW_MAJOR && a.la != GE_COL_MAJOR) || (a.lb != GE_ROW_MAJOR && a.lb != GE_COL_MAJOR))
+        return fail(GE_ERR_INVALID_VALUE, "layout must be GE_ROW_MAJOR or GE_COL_MAJOR");
+    if (a.op < GE_EPI_NONE || a.op > GE_EPI_BIAS_RELU) return fail(GE_ERR_INVALID_VALUE, "bad epilogue op");
+    const ge_options& o = a.o;
+    if (o.bias_mode < GE_BIAS_ROW || o.bias_mode > GE_BIAS_FULL) return fail(GE_ERR_INVALID_VALUE, "bad bias_mode");
+    if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_RELU) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
+    if (o.out_dtype != GE_OUT_F16 && o.out_dtype != GE_OUT_F32) return fail(GE_ERR_INVALID_VALUE, "bad out_dtype");
+    if (o.tile_n != 0 && o.tile_n != 64 && o.tile_n != 128 && o.tile_n != 256)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128 or 256");
+    if (o.cta_group < 0 || o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
+    if (o.cta_group == 2 && o.tile_n == 64) return fail(GE_ERR_INVALID_VALUE, "cta_group 2 needs tile_n 128 or 256");
+    // packed defaults
+    const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
+    const int64_t minlda = arow ? a.K : a.M, minldb = brow ? a.N : a.K;
+    if (a.lda == 0) a.lda = std::max<int64_t>(minlda, 1);
+    if (a.ldb == 0) a.ldb = std::max<int64_t>(minldb, 1);
+    if (a.ldc == 0) a.ldc = std::max<int64_t>(a.N, 1);
+    if (a.lda < minlda || a.ldb < minldb || a.ldc < a.N || a.lda < 0 || a.ldb < 0 || a.ldc < 0) {
+        snprintf(buf, sizeof buf, "leading dimension too small (lda=%lld ldb=%lld ldc=%lld)", (long long)a.lda,
+                 (long long)a.ldb, (long long)a.ldc);
+        return fail(GE_ERR_INVALID_VALUE, buf);
+    }
+    const int64_t outerA = arow ? a.M : a.K, outerB = brow ? a.K : a.N;
+    if (a.sA == 0) a.sA = outerA * a.lda;
+    if (a.sB == 0) a.sB = outerB * a.ldb;
+    if (a.sC == 0) a.sC = a.M * a.ldc;
+    if (a.o.bias_mode == GE_BIAS_FULL && a.o.ldbias == 0) a.o.ldbias = a.N;
+    if (a.sA < 0 || a.sB < 0 || a.sC < 0 || a.sBias < 0 || a.o.ldbias < 0)
+        return fail(GE_ERR_INVALID_VALUE, "negative stride");
+    if (a.o.bias_mode == GE_BIAS_FULL && a.o.ldbias < a.N) return fail(GE_ERR_INVALID_VALUE, "ldbias < N");
+    if (a.batch > 1 && a.sC < a.M * a.ldc)
+        return fail(GE_ERR_INVALID_VALUE, "strideC smaller than one output item (items would overlap)");
+    if (a.batch == 0 || a.M == 0 || a.N == 0) return GE_OK;   // no-op
+    if (!a.C) return fail(GE_ERR_INVALID_VALUE, "C is NULL");
+    if (a.K > 0 && (!a.A || !a.B)) return fail(GE_ERR_INVALID_VALUE, "A or B is NULL");
+    if (has_bias(a.op) && !a.bias) return fail(GE_ERR_INVALID_VALUE, "bias is NULL but the op adds a bias");
+    if (a.o.prologue == GE_PRO_SCALE_K && a.K > 0 && !a.o.prologue_scale)
+        return fail(GE_ERR_INVALID_VALUE, "prologue_scale is NULL for GE_PRO_SCALE_K");
+    if (a.K > 0) {
+        if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15))
+            return fail(GE_ERR_MISALIGNED, "A and B must be 16-byte aligned (TMA)");
+        if ((a.lda * 2) % 16 || (a.ldb * 2) % 16)
+            return fail(GE_ERR_MISALIGNED, "lda and ldb must be multiples of 8 elements (16 bytes, TMA)");
+        if (a.batch > 1 && ((a.sA * 2) % 16 || (a.sB * 2) % 16))
+            return fail(GE_ERR_MISALIGNED, "strideA and strideB must be multiples of 8 elements (TMA)");
+        if (a.batch > 1 && (a.sA == 0 || a.sB == 0))
+            return fail(GE_ERR_INVALID_VALUE, "strideA/strideB must be positive for batch > 1");
+    }
+    // aliasing: C must not overlap any input
+    const int es = a.o.out_dtype == GE_OUT_F32 ? 4 : 2;
+    const int64_t nC = extent_bytes(a.batch, a.M, a.N, a.ldc, a.sC, es);
+    const int64_t nA = extent_bytes(a.batch, outerA, arow ? a.K : a.M, a.lda, a.sA, 2);
+    const int64_t nB = extent_bytes(a.batch, outerB, brow ? a.N : a.K, a.ldb, a.sB, 2);
+    int64_t nBias = 0;
+    if (has_bias(a.op)) {
+        if (a.o.bias_mode == GE_BIAS_ROW) nBias = ((a.batch - 1) * a.sBias + a.N) * 2;
+        else if (a.o.bias_mode == GE_BIAS_COL) nBias = ((a.batch - 1) * a.sBias + a.M) * 2;
+        else nBias = extent_bytes(a.batch, a.M, a.N, a.o.ldbias, a.sBias, 2);
+    }
+    const int64_t nS = (a.o.prologue == GE_PRO_SCALE_K) ? a.K * 4 : 0;
+    if (overlap(a.C, nC, a.A, a.K ? nA : 0) || overlap(a.C, nC, a.B, a.K ? nB : 0) ||
+        overlap(a.C, nC, a.bias, nBias) || overlap(a.C, nC, a.o.prologue_scale, nS))
+        return fail(GE_ERR_ALIASING, "C overlaps an input buffer");
+    return GE_OK;
+}
+
+// ------------------------------------------------------------------ plan
+struct Plan {
+    int bn, cg, stages;
+    int64_t tiles;
+};
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+Plan make_plan(const Args& a, int sms) {
+    Plan p{};
+    int cg = a.o.cta_group;
+    int bn = a.o.tile_n;
+    auto tiles = [&](int bn_, int cg_) { return a.batch * cdiv(a.M, 128 * cg_) * cdiv(a.N, bn_); };
+    if (cg == 0) cg = 1;          // heuristic refined by measurement
+    if (bn == 0) {
+        bn = 256;
+        // narrow the N tile while the grid would leave most SMs idle (skinny / small problems)
+        while (bn > (cg == 2 ? 128 : 64) && tiles(bn, cg) * cg < sms) bn /= 2;
+        if (cg == 2 && bn < 128) bn = 128;
+    }
+    p.bn = bn;
+    p.cg = cg;
+    p.tiles = tiles(bn, cg);
+    p.stages = ge::stages_for(bn, cg);
+    return p;
+}
+
+// ------------------------------------------------------------------ tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+// 3-D map {inner, outer, batch} with 128-B swizzle; OOB elements load as zero, stores clip.
+bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, int64_t inner, int64_t outer,
+              int64_t batch, int64_t ld, int64_t stride, uint32_t box_inner, uint32_t box_outer) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)batch};
+    // byte strides of dims 1 and 2; a 1-item batch gets a harmless non-zero stride
+    int64_t s2 = batch > 1 ? stride * es : ld * es * std::max<int64_t>(outer, 1);
+    cuuint64_t strides[2] = {(cuuint64_t)(ld * es), (cuuint64_t)s2};
+    cuuint32_t box[3] = {box_inner, box_outer, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+ge_status launch(Args& a, cudaStream_t st) {
+    ge_status s = validate(a);
+    if (s != GE_OK) return s;
+    if (a.batch == 0 || a.M == 0 || a.N == 0) return GE_OK;
+    int sms = 0;
+    s = device_info(&sms);
+    if (s != GE_OK) return s;
+    const Plan pl = make_plan(a, sms);
+    const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
+    const bool a_mn = !arow, b_mn = brow;          // row-major A is K-major; row-major B is N(MN)-major
+    const bool f32 = a.o.out_dtype == GE_OUT_F32;
+    const bool pro = a.o.prologue != GE_PRO_NONE;
+    const int es = f32 ? 4 : 2;
+
+    ge::Maps maps;
+    std::memset(&maps, 0, sizeof maps);
+    if (a.K > 0) {
+        bool ok;
+        if (!a_mn) ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.K, a.M, a.batch, a.lda, a.sA, 64, 128);
+        else ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.M, a.K, a.batch, a.lda, a.sA, 64, 64);
+        if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for A");
+        const uint32_t brows = static_cast<uint32_t>(pl.bn / pl.cg);
+        if (!b_mn) ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.K, a.N, a.batch, a.ldb, a.sB, 64, brows);
+        else ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.N, a.K, a.batch, a.ldb, a.sB, 64, 64);
+        if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for B");
+    }
+    const bool c_tma = (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && ((a.ldc * es) % 16 == 0) &&
+                       (a.batch == 1 || (a.sC * es) % 16 == 0);
+    if (c_tma) {
+        if (!encode3d(&maps.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, es, a.C, a.N,
+                      a.M, a.batch, a.ldc, a.sC, f32 ? 32 : 64, 32))
+            return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for C");
+    }
+
+    ge::Params p{};
+    p.M = static_cast<int>(a.M);
+    p.N = static_cast<int>(a.N);
+    p.K = static_cast<int>(a.K);
+    p.batch = static_cast<int>(a.batch);
+    p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg));
+    p.num_n_tiles = static_cast<int>(cdiv(a.N, pl.bn));
+    p.num_k_blocks = static_cast<int>(cdiv(a.K, ge::kBK));
+    p.group_m = 16;
+    p.num_tiles = pl.tiles;
+    p.bias = has_bias(a.op) ? static_cast<const __half*>(a.bias) : nullptr;
+    p.bias_mode = has_bias(a.op) ? a.o.bias_mode : ge::BIAS_NONE;
+    p.ldbias = a.o.ldbias;
+    p.stride_bias = a.sBias;
+    p.bias_vec = p.bias && (reinterpret_cast<uintptr_t>(p.bias) % 16 == 0) && (a.sBias % 8 == 0) &&
+                 (a.o.bias_mode != GE_BIAS_FULL || a.o.ldbias % 8 == 0);
+    p.relu = has_relu(a.op) ? 1 : 0;
+    p.scale = a.o.prologue == GE_PRO_SCALE_K ? a.o.prologue_scale : nullptr;
+    p.prologue = a.o.prologue;
+    p.scale_vec = p.scale && (reinterpret_cast<uintptr_t>(p.scale) % 16 == 0);
+    p.C = a.C;
+    p.ldc = a.ldc;
+    p.stride_c = a.sC;
+    p.c_tma = c_tma ? 1 : 0;
+
+    const int64_t clusters = std::min<int64_t>(pl.tiles, sms / pl.cg);
+    const int grid = static_cast<int>(std::max<int64_t>(clusters, 1) * pl.cg);
+    cudaError_t e;
+    if (pl.cg == 1) {
+        if (pl.bn == 64) e = ge::launch_cg1_bn64(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else if (pl.bn == 128) e = ge::launch_cg1_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg1_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
+    } else {
+        if (pl.bn == 128) e = ge::launch_cg2_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg2_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GE_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return GE_OK;
+}
+
+Args make_args(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t la, int32_t lb, const void* A, int64_t lda,
+               int64_t sA, const void* B, int64_t ldb, int64_t sB, const void* bias, int64_t sBias, void* C,
+               int64_t ldc, int64_t sC, int32_t op, const ge_options* opt) {
+    Args a{batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op, {}};
+    if (opt) a.o = *opt;
+    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0};
+    return a;
+}
+
+// ------------------------------------------------------------------ host-buffer workspace
+struct Workspace {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_ws_mu;
+Workspace g_ws[64];
+
+}  // namespace
+
+namespace ge {
+int smem_bytes_for(int bn, int cg) {
+    if (cg == 1) return bn == 64 ? Cfg<64, 1>::kSmemBytes : bn == 128 ? Cfg<128, 1>::kSmemBytes : Cfg<256, 1>::kSmemBytes;
+    return bn == 128 ? Cfg<128, 2>::kSmemBytes : Cfg<256, 2>::kSmemBytes;
+}
+int stages_for(int bn, int cg) {
+    if (cg == 1) return bn == 64 ? Cfg<64, 1>::kStages : bn == 128 ? Cfg<128, 1>::kStages : Cfg<256, 1>::kStages;
+    return bn == 128 ? Cfg<128, 2>::kStages : Cfg<256, 2>::kStages;
+}
+}  // namespace ge
+
+extern "C" {
+
+ge_status gemm_epilogue(int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, const void* bias, void* C, int64_t ldc, int32_t op,
+                        const ge_options* opt, void* stream) {
+    Args a = make_args(1, M, N, K, layoutA, layoutB, A, lda, 0, B, ldb, 0, bias, 0, C, ldc, 0, op, opt);
+    g_detail.clear();
+    return launch(a, static_cast<cudaStream_t>(stream));
+}
+
+ge_status gemm_epilogue_batched(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
+                                const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb,
+                                int64_t strideB, const void* bias, int64_t strideBias, void* C, int64_t ldc,
+                                int64_t strideC, int32_t op, const ge_options* opt, void* stream) {
+    Args a = make_args(batch, M, N, K, layoutA, layoutB, A, lda, strideA, B, ldb, strideB, bias, strideBias, C, ldc,
+                       strideC, op, opt);
+    g_detail.clear();
+    return launch(a, static_cast<cudaStream_t>(stream));
+}
+
+ge_status ge_validate(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB, const void* A,
+                      int64_t lda, int64_t strideA, const void* B, int64_t ldb, int64_t strideB, const void* bias,
+                      int64_t strideBias, void* C, int64_t ldc, int64_t strideC, int32_t op, const ge_options* opt) {
+    Args a = make_args(batch, M, N, K, layoutA, layoutB, A, lda, strideA, B, ldb, strideB, bias, strideBias, C, ldc,
+                       strideC, op, opt);
+    g_detail.clear();
+    return validate(a);
+}
+
+ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
+                             const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb, int64_t strideB,
+                             const void* bias, int64_t strideBias, void* C, int64_t ldc, int64_t strideC, int32_t op,
+                             const ge_options* opt, void* stream) {
+    g_detail.clear();
+    Args a = make_args(batch, M, N, K, layoutA, layoutB, A, lda, strideA, B, ldb, strideB, bias, strideBias, C, ldc,
+                       strideC, op, opt);
+    ge_status s = validate(a);
+    if (s != GE_OK) return s;
+    if (a.batch == 0 || a.M == 0 || a.N == 0) return GE_OK;
+    int sms = 0;
+    s = device_info(&sms);
+    if (s != GE_OK) return s;
+    const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
+    const int es = a.o.out_dtype == GE_OUT_F32 ? 4 : 2;
+    const int64_t nA = a.K ? extent_bytes(a.batch, arow ? a.M : a.K, arow ? a.K : a.M, a.lda, a.sA, 2) : 0;
+    const int64_t nB = a.K ? extent_bytes(a.batch, brow ? a.K : a.N, brow ? a.N : a.K, a.ldb, a.sB, 2) : 0;
+    int64_t nBias = 0;
+    if (has_bias(a.op)) {
+        if (a.o.bias_mode == GE_BIAS_ROW) nBias = ((a.batch - 1) * a.sBias + a.N) * 2;
+        else if (a.o.bias_mode == GE_BIAS_COL) nBias = ((a.batch - 1) * a.sBias + a.M) * 2;
+        else nBias = extent_bytes(a.batch, a.M, a.N, a.o.ldbias, a.sBias, 2);
+    }
+    const int64_t nS = (a.o.prologue == GE_PRO_SCALE_K && a.K) ? a.K * 4 : 0;
+    const int64_t nC = extent_bytes(a.batch, a.M, a.N, a.ldc, a.sC, es);
+    auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
+    const size_t need = up(nA) + up(nB) + up(nBias) + up(nS) + up(nC);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace& ws = g_ws[dev & 63];
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ws.bytes < need) {
+        if (ws.ptr) {
+            cudaStreamSynchronize(st);
+            cudaFree(ws.ptr);
+        }
+        ws.ptr = nullptr;
+        ws.bytes = 0;
+        if (cudaMalloc(&ws.ptr, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(GE_ERR_CUDA, "workspace cudaMalloc failed");
+        }
+        ws.bytes = need;
+    }
+    char* base = static_cast<char*>(ws.ptr);
+    char* dA = base;
+    char* dB = dA + up(nA);
+    char* dBias = dB + up(nB);
+    char* dS = dBias + up(nBias);
+    char* dC = dS + up(nS);
+    cudaError_t e = cudaSuccess;
+    if (nA) e = cudaMemcpyAsync(dA, a.A, nA, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && nB) e = cudaMemcpyAsync(dB, a.B, nB, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && nBias) e = cudaMemcpyAsync(dBias, a.bias, nBias, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && nS) e = cudaMemcpyAsync(dS, a.o.prologue_scale, nS, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GE_ERR_CUDA, std::string("H2D copy failed: ") + cudaGetErrorString(e));
+    }
+    Args d = a;
+    d.A = nA ? dA : nullptr;
+    d.B = nB ? dB : nullptr;
+    d.bias = nBias ? dBias : nullptr;
+    d.o.prologue_scale = nS ? reinterpret_cast<const float*>(dS) : nullptr;
+    d.C = dC;
+    s = launch(d, st);
+    if (s != GE_OK) return s;
+    // copy back only the M x N elements of each item (the caller's padding is left untouched)
+    for (int64_t b = 0; b < a.batch && e == cudaSuccess; ++b)
+        e = cudaMemcpy2DAsync(static_cast<char*>(a.C) + b * a.sC * es, a.ldc * es, dC + b * a.sC * es, a.ldc * es,
+                              a.N * es, a.M, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GE_ERR_CUDA, std::string("host path failed: ") + cudaGetErrorString(e));
+    }
+    return GE_OK;
+}
+
+ge_status ge_release_workspace(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GE_ERR_UNSUPPORTED_DEVICE, "no CUDA device");
+    }
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace& ws = g_ws[dev & 63];
+    if (ws.ptr) {
+        cudaDeviceSynchronize();
+        cudaFree(ws.ptr);
+    }
+    ws.ptr = nullptr;
+    ws.bytes = 0;
+    return GE_OK;
+}
+
+const char* ge_status_string(ge_status s) {
+    switch (s) {
+    case GE_OK: return "GE_OK";
+    case GE_ERR_INVALID_VALUE: return "GE_ERR_INVALID_VALUE: invalid argument";
+    case GE_ERR_MISALIGNED: return "GE_ERR_MISALIGNED: operand breaks the 16-byte TMA alignment rules";
+    case GE_ERR_ALIASING: return "GE_ERR_ALIASING: output overlaps an input";
+    case GE_ERR_UNSUPPORTED_DEVICE: return "GE_ERR_UNSUPPORTED_DEVICE: needs an sm_100 (B200) device";
+    case GE_ERR_CUDA: return "GE_ERR_CUDA: CUDA call failed";
+    }
+    return "unknown ge_status";
+}
+
+const char* ge_last_error_detail(void) { return g_detail.c_str(); }
+
+ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
+                  const ge_options* opt, int32_t num_sms, int32_t* tile_m, int32_t* tile_n, int32_t* cta_group,
+                  int32_t* stages, int64_t* num_tiles) {
+    g_detail.clear();
+    Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0,
+                       GE_EPI_NONE, opt);
+    if (batch < 0 || M < 0 || N < 0 || K < 0 || num_sms <= 0) return fail(GE_ERR_INVALID_VALUE, "bad plan arguments");
+    if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 256)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128 or 256");
+    if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
+    const Plan p = make_plan(a, num_sms);
+    if (tile_m) *tile_m = 128 * p.cg;
+    if (tile_n) *tile_n = p.bn;
+    if (cta_group) *cta_group = p.cg;
+    if (stages) *stages = p.stages;
+    if (num_tiles) *num_tiles = p.tiles;
+    return GE_OK;
+}
+
+uint64_t ge_launch_count(void) { return g_launches.load(); }
+
+const char* ge_version(void) { return "gemm_epilogue-b200 0.1.0 (sm_100a, tcgen05/TMA/TMEM)"; }
+
+}  // extern "C"

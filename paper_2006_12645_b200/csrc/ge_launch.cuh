@@ -1,0 +1,80 @@
+// ge_launch.cuh -- per-configuration launchers (instantiated in ge_inst_*.cu, dispatched by ge_api.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ge_kernel.cuh"
+
+namespace ge {
+
+struct Maps {
+    CUtensorMap a, b, c;
+};
+
+// Smem bytes the (BN, CG) configuration requests (host and device agree through Cfg).
+int smem_bytes_for(int bn, int cg);
+int stages_for(int bn, int cg);
+
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG>
+cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st) {
+    auto kern = ge_fused_kernel<BN, A_MN, B_MN, OUT_F32, PRO, CG>;
+    constexpr int smem = Cfg<BN, CG>::kSmemBytes;
+    static bool attr_done = false;   // benign race: setting the attribute twice is harmless
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(PRO ? 384 : 256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.c, p);
+}
+
+// Dispatch over the 16 (A_MN, B_MN, OUT_F32, PRO) variants of one (BN, CG) configuration.
+template <int BN, int CG>
+cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m, const Params& p, int grid,
+                         cudaStream_t st) {
+    const int key = (a_mn ? 8 : 0) | (b_mn ? 4 : 0) | (f32 ? 2 : 0) | (pro ? 1 : 0);
+    switch (key) {
+#define GE_CASE(K, AM, BM, F, P) \
+    case K: return launch_one<BN, AM, BM, F, P, CG>(m, p, grid, st);
+        GE_CASE(0, false, false, false, false)
+        GE_CASE(1, false, false, false, true)
+        GE_CASE(2, false, false, true, false)
+        GE_CASE(3, false, false, true, true)
+        GE_CASE(4, false, true, false, false)
+        GE_CASE(5, false, true, false, true)
+        GE_CASE(6, false, true, true, false)
+        GE_CASE(7, false, true, true, true)
+        GE_CASE(8, true, false, false, false)
+        GE_CASE(9, true, false, false, true)
+        GE_CASE(10, true, false, true, false)
+        GE_CASE(11, true, false, true, true)
+        GE_CASE(12, true, true, false, false)
+        GE_CASE(13, true, true, false, true)
+        GE_CASE(14, true, true, true, false)
+        GE_CASE(15, true, true, true, true)
+#undef GE_CASE
+    }
+    return cudaErrorInvalidValue;
+}
+
+// Defined in ge_inst_*.cu (one translation unit per configuration, compiled in parallel).
+cudaError_t launch_cg1_bn64(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+
+}  // namespace ge

@@ -1,0 +1,169 @@
+"""CPU-side tests of the C ABI library: it builds, loads, exports every symbol that
+include/gemm_epilogue.h declares, validates arguments exactly as documented, plans tiles, and
+fails loudly (no CPU fallback) when there is no sm_100 device.  No kernel is launched here."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from paper_2006_12645_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gemm_epilogue.h")
+
+
+@pytest.fixture(scope="module")
+def ge():
+    _build.build()
+    import paper_2006_12645_b200 as ge
+    ge.load_library()
+    return ge
+
+
+@pytest.fixture(scope="module")
+def lib(ge):
+    return ge.load_library()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(?:ge_status|uint64_t|const char\*)\s+(\w+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert {"gemm_epilogue", "gemm_epilogue_batched", "gemm_epilogue_host", "ge_validate", "ge_status_string",
+            "ge_last_error_detail", "ge_plan", "ge_launch_count", "ge_version",
+            "ge_release_workspace"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_library_is_sm100a_native(lib):
+    """The .so carries sm_100a SASS with tcgen05 MMA, TMEM loads and TMA (B200_PROFILING.md table)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "-sass", _build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UTMASTG"):
+        assert mnem in out, mnem
+    assert "HMMA.16816" not in out          # no legacy mma.sync path
+
+
+def test_strings(lib):
+    for s in range(6):
+        assert lib.ge_status_string(s).startswith(b"GE_")
+    assert lib.ge_status_string(99) == b"unknown ge_status"
+    assert b"sm_100a" in lib.ge_version()
+
+
+# ------------------------------------------------------------------ validation matrix
+P = 0x10000          # fake, 16-byte aligned, never dereferenced (ge_validate only compares pointers)
+
+
+def v(lib, batch=1, M=128, N=128, K=64, la=0, lb=0, A=P, lda=0, sA=0, B=P * 16, ldb=0, sB=0, bias=P * 64, sBias=0,
+      C=P * 128, ldc=0, sC=0, op=3, opt=None):
+    return lib.ge_validate(batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op,
+                           ctypes.byref(opt) if opt is not None else None)
+
+
+def opts(ge, **kw):
+    o = ge.GEOptions()
+    o.bias_mode, o.ldbias, o.prologue, o.prologue_scale, o.out_dtype, o.tile_n, o.cta_group = 0, 0, 0, None, 0, 0, 0
+    for k, val in kw.items():
+        setattr(o, k, val)
+    return o
+
+
+def test_validate_ok(lib, ge):
+    assert v(lib) == 0
+    for la in (0, 1):
+        for lb in (0, 1):
+            assert v(lib, la=la, lb=lb) == 0
+    assert v(lib, M=0) == 0 and v(lib, N=0) == 0 and v(lib, batch=0) == 0      # no-ops
+    assert v(lib, K=0, A=0, B=0) == 0                                           # K = 0: A/B unused
+
+
+def test_validate_invalid_values(lib, ge):
+    S = ge.Status
+    assert v(lib, M=-1) == S.INVALID_VALUE
+    assert v(lib, K=-5) == S.INVALID_VALUE
+    assert v(lib, batch=-1) == S.INVALID_VALUE
+    assert v(lib, M=1 << 31) == S.INVALID_VALUE
+    assert v(lib, la=2) == S.INVALID_VALUE
+    assert v(lib, op=4) == S.INVALID_VALUE
+    assert v(lib, lda=32) == S.INVALID_VALUE            # row-major A needs lda >= K = 64
+    assert v(lib, la=1, lda=64) == S.INVALID_VALUE      # col-major A needs lda >= M = 128
+    assert v(lib, ldb=64) == S.INVALID_VALUE            # row-major B needs ldb >= N
+    assert v(lib, ldc=100) == S.INVALID_VALUE
+    assert v(lib, C=0) == S.INVALID_VALUE
+    assert v(lib, A=0) == S.INVALID_VALUE
+    assert v(lib, bias=0) == S.INVALID_VALUE            # op has a bias
+    assert v(lib, bias=0, op=2) == 0                    # relu only: no bias needed
+    assert v(lib, opt=opts(ge, bias_mode=3)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, prologue=1)) == S.INVALID_VALUE          # SCALE_K without a scale
+    assert v(lib, opt=opts(ge, prologue=1, prologue_scale=P * 512)) == 0
+    assert v(lib, opt=opts(ge, out_dtype=2)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, tile_n=96)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, cta_group=3)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, cta_group=2, tile_n=64)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, bias_mode=2, ldbias=64)) == S.INVALID_VALUE   # ldbias < N
+    assert v(lib, batch=2, sC=100) == S.INVALID_VALUE   # output items would overlap
+    assert lib.ge_last_error_detail()                    # a reason is recorded
+
+
+def test_validate_alignment(lib, ge):
+    S = ge.Status
+    assert v(lib, A=P + 2) == S.MISALIGNED
+    assert v(lib, B=P * 16 + 8) == S.MISALIGNED
+    assert v(lib, K=60, lda=60) == S.MISALIGNED          # 120-byte rows break the TMA stride rule
+    assert v(lib, batch=2, sA=128 * 64 + 4) == S.MISALIGNED
+    assert v(lib, C=P * 128 + 2) == 0                    # C/bias have a st.global fallback
+    assert v(lib, N=37, ldc=37, ldb=40) == 0
+
+
+def test_validate_aliasing(lib, ge):
+    S = ge.Status
+    assert v(lib, C=P) == S.ALIASING                     # C == A
+    assert v(lib, C=P * 16 + 64) == S.ALIASING           # C inside B
+    assert v(lib, C=P * 64) == S.ALIASING                # C == bias
+    assert v(lib, C=P * 64 - 2 * 128 * 128 + 2) == S.ALIASING   # C's tail overlaps bias
+
+
+def test_plan_tiles(ge):
+    p = ge.plan(8192, 8192, 8192, tile_n=256, cta_group=1)
+    assert p["tile_m"] == 128 and p["tile_n"] == 256 and p["num_tiles"] == 64 * 32
+    p = ge.plan(8192, 8192, 8192, tile_n=256, cta_group=2)
+    assert p["tile_m"] == 256 and p["num_tiles"] == 32 * 32
+    p = ge.plan(35, 8457, 2560)                        # skinny: heuristic narrows the N tile to fill the SMs
+    assert p["tile_n"] == 64 and p["num_tiles"] == 133
+    p = ge.plan(2048, 2048, 2048, batch=64)
+    assert p["num_tiles"] >= 64 * 16 * 8
+    assert p["stages"] >= 4
+
+
+def test_no_device_fails_loudly(ge):
+    """Without an sm_100 device the product raises; it never computes on the CPU."""
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    A = torch.zeros((64, 64), dtype=torch.float16)
+    with pytest.raises(Exception):
+        ge.gemm_epilogue(A, A)
+
+
+def test_binding_layout_detection(ge):
+    X = torch.zeros((96, 40), dtype=torch.float16)
+    assert ge.layout_of(X) == (0, 40)
+    assert ge.layout_of(X.t()) == (1, 40)
+    Y = torch.zeros((96, 48), dtype=torch.float16)[:, :40]
+    assert ge.layout_of(Y) == (0, 48)
+    with pytest.raises(ValueError):
+        ge.layout_of(torch.zeros((8, 8, 2), dtype=torch.float16)[:, :, 0])

@@ -1,0 +1,201 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerance (BASELINE.json north_star): |gpu - oracle| <= 4e-3*mag + 1e-3*|oracle| per element,
+mag = sum_k |a'_ik b_kj|.  Small-integer data is exact in fp32 in any summation order, so there
+the GPU must equal RNE_fp16(oracle) (fp16 out) or the oracle itself (fp32 out) bitwise
+(DESIGN.md "Parity").  All inputs are seeded (workloads.py)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from tests.helpers import check_bound, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+ge = pytest.importorskip("paper_2006_12645_b200")
+
+
+def dev_operands(prob: workloads.Problem, layouts: str, lda=None, ldb=None):
+    """Logical views on the GPU whose storage follows the layout pair (row/col major, padded ld)."""
+    def put(logical, lay, ld):
+        st, ld = workloads.store(logical, lay, ld)
+        d = st.cuda()
+        R, C = logical.shape
+        return d[:, :C] if lay == "r" else d[:, :R].t()
+    return put(prob.A, layouts[0], lda), put(prob.B, layouts[1], ldb)
+
+
+def run_gpu(prob, layouts="rr", *, op=None, out_dtype=torch.float16, lda=None, ldb=None, **kw):
+    A, B = dev_operands(prob, layouts, lda, ldb)
+    bias = prob.bias.cuda() if prob.bias is not None else None
+    scale = prob.scale.cuda() if prob.scale is not None else None
+    C = ge.gemm_epilogue(A, B, bias, op=op, bias_mode=prob.meta.get("bias_mode") or "row",
+                         prologue=prob.meta.get("prologue"), scale=scale, out_dtype=out_dtype, **kw)
+    torch.cuda.synchronize()
+    return C.float().cpu().numpy().astype(np.float64)
+
+
+def exact_expect(out, out_dtype):
+    return out if out_dtype == torch.float32 else oracle.f16_decode(oracle.f16_encode(out))
+
+
+CONFIGS = [(64, 1), (128, 1), (256, 1), (128, 2), (256, 2)]
+
+
+# ------------------------------------------------------------------ small full-matrix parity
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+@pytest.mark.parametrize("kind", ["uniform", "smallint"])
+def test_layouts_ragged(layouts, kind):
+    """All four layouts on a ragged 300x520x200 problem spanning several tiles."""
+    prob = workloads.make_problem(300, 520, 200, seed=31, kind=kind, bias_mode="row")
+    got = run_gpu(prob, layouts)
+    out, mag = oracle_run(prob, layouts)
+    if kind == "smallint":
+        assert np.array_equal(got, exact_expect(out, torch.float16))
+    else:
+        check_bound(got, out, mag, layouts)
+
+
+@pytest.mark.parametrize("tile_n,cg", CONFIGS)
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_tile_configs_exact(tile_n, cg, layouts):
+    """Every kernel configuration (N tile 64/128/256, 1-CTA and CTA-pair) is bitwise exact on
+    small-integer data, with M/N/K tails (M=333, N=777, K=321)."""
+    prob = workloads.make_problem(333, 777, 321, seed=32, kind="smallint", bias_mode="row")
+    got = run_gpu(prob, layouts, tile_n=tile_n, cta_group=cg)
+    out, _ = oracle_run(prob, layouts)
+    assert np.array_equal(got, exact_expect(out, torch.float16))
+
+
+@pytest.mark.parametrize("bias_mode", ["row", "col", "full"])
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.float32])
+@pytest.mark.parametrize("op", ["none", "bias", "relu", "bias_relu"])
+def test_epilogue_variants(bias_mode, out_dtype, op):
+    """Bias modes (DESIGN.md R-C2), epilogue ops and fp16/fp32 outputs, exact on small integers."""
+    prob = workloads.make_problem(200, 300, 130, seed=33, kind="smallint", bias_mode=bias_mode,
+                                  ldbias=312 if bias_mode == "full" else None)
+    got = run_gpu(prob, "rc", op=op, out_dtype=out_dtype)
+    use_bias = op in ("bias", "bias_relu")
+    out, _ = oracle_run(prob, "rc", relu=op in ("relu", "bias_relu"), bias_mode=bias_mode if use_bias else "none")
+    assert np.array_equal(got, exact_expect(out, out_dtype))
+
+
+@pytest.mark.parametrize("prologue", ["scale_k", "relu"])
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+@pytest.mark.parametrize("tile_n,cg", [(256, 1), (256, 2), (64, 1)])
+def test_prologue(prologue, layouts, tile_n, cg):
+    """Prologue fusion (Sec. VII-C; SCALE_K = DESIGN.md R-C12): exact on small
+    integers with s in {0.5, 1, 2}, within the bound on uniform data."""
+    for kind in ("smallint", "uniform"):
+        prob = workloads.make_problem(257, 300, 200, seed=34, kind=kind, bias_mode="row", prologue=prologue)
+        got = run_gpu(prob, layouts, tile_n=tile_n, cta_group=cg)
+        out, mag = oracle_run(prob, layouts)
+        if kind == "smallint":
+            assert np.array_equal(got, exact_expect(out, torch.float16))
+        else:
+            check_bound(got, out, mag, f"{prologue} {layouts}")
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 8), (1, 300, 64), (300, 1, 64), (127, 129, 63), (128, 256, 64),
+                                   (129, 257, 65), (64, 64, 4096), (1000, 72, 17)])
+def test_odd_shapes(M, N, K):
+    prob = workloads.make_problem(M, N, K, seed=35, kind="smallint", bias_mode="row")
+    for lay in ("rr", "cc"):
+        got = run_gpu(prob, lay)
+        out, _ = oracle_run(prob, lay)
+        assert np.array_equal(got, exact_expect(out, torch.float16)), lay
+
+
+def test_k_zero_and_empty():
+    """K = 0 gives op(bias) (DESIGN.md R-C9); M = 0 / N = 0 are no-ops."""
+    prob = workloads.make_problem(70, 90, 0, seed=36, bias_mode="col")
+    got = run_gpu(prob, "rr")
+    b = prob.bias.float().numpy().astype(np.float64)[:, None] + np.zeros((70, 90))
+    assert np.array_equal(got, np.where(b > 0, b, 0.0))
+    A = torch.zeros((0, 64), dtype=torch.float16, device="cuda")
+    B = torch.zeros((64, 32), dtype=torch.float16, device="cuda")
+    assert ge.gemm_epilogue(A, B).shape == (0, 32)
+
+
+def test_padded_ld_and_c_fallback():
+    """Padded lda/ldb; a C whose ldc breaks the 16-byte TMA rule goes through the st.global epilogue
+    (the DeepBench N = 8457 case)."""
+    prob = workloads.make_problem(150, 37, 100, seed=37, kind="smallint", bias_mode="row")
+    A, B = dev_operands(prob, "cr", lda=160, ldb=40)
+    Cbuf = torch.full((150, 37), 7.0, dtype=torch.float16, device="cuda")       # ldc = 37: misaligned rows
+    ge.gemm_epilogue(A, B, prob.bias.cuda(), out=Cbuf)
+    torch.cuda.synchronize()
+    out, _ = oracle_run(prob, "cr")
+    assert np.array_equal(Cbuf.float().cpu().numpy(), exact_expect(out, torch.float16))
+    # misaligned base pointer of C (offset by one element) and fp32 output
+    big = torch.zeros(150 * 40 + 1, dtype=torch.float32, device="cuda")
+    Cv = big[1:].view(150, 40)[:, :37]
+    ge.gemm_epilogue(A, B, prob.bias.cuda(), out=Cv)
+    torch.cuda.synchronize()
+    assert np.array_equal(Cv.cpu().numpy().astype(np.float64), out)
+
+
+def test_padding_untouched():
+    """Only the M x N window of C is written (ldc > N, the padding keeps its contents)."""
+    prob = workloads.make_problem(130, 200, 64, seed=38, kind="smallint", bias_mode="row")
+    A, B = dev_operands(prob, "rr")
+    Cbuf = torch.full((130, 256), -5.0, dtype=torch.float16, device="cuda")
+    ge.gemm_epilogue(A, B, prob.bias.cuda(), out=Cbuf[:, :200])
+    torch.cuda.synchronize()
+    assert (Cbuf[:, 200:] == -5.0).all()
+
+
+@pytest.mark.parametrize("shared_bias", [True, False])
+def test_batched_matches_single(shared_bias):
+    """Item b of the batched call equals the single call on item b, bitwise (DESIGN.md R-C14)."""
+    batch, M, N, K = 5, 200, 136, 96
+    probs = [workloads.make_problem(M, N, K, seed=400 + b, bias_mode="row") for b in range(batch)]
+    A = torch.stack([p.A for p in probs]).cuda()
+    B = torch.stack([p.B for p in probs]).cuda().transpose(1, 2).contiguous().transpose(1, 2)  # col-major items
+    bias = probs[0].bias.cuda() if shared_bias else torch.stack([p.bias for p in probs]).cuda()
+    C = ge.gemm_epilogue_batched(A, B, bias)
+    for b in range(batch):
+        Cb = ge.gemm_epilogue(A[b], B[b], bias if shared_bias else bias[b])
+        torch.cuda.synchronize()
+        assert torch.equal(C[b], Cb)
+        p = probs[b]
+        if shared_bias:
+            p = workloads.Problem(M, N, K, p.A, p.B, probs[0].bias, None, p.meta)
+        out, mag = oracle_run(p, "rc")
+        check_bound(C[b].float().cpu().numpy(), out, mag, f"item {b}")
+
+
+def test_deterministic():
+    prob = workloads.make_problem(512, 512, 512, seed=39, bias_mode="row")
+    A, B = dev_operands(prob, "rr")
+    bias = prob.bias.cuda()
+    c1 = ge.gemm_epilogue(A, B, bias)
+    c2 = ge.gemm_epilogue(A, B, bias)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+
+
+def test_errors_raise():
+    A = torch.zeros((64, 64), dtype=torch.float16, device="cuda")
+    B = torch.zeros((64, 64), dtype=torch.float16, device="cuda")
+    with pytest.raises(ge.GEError) as e:
+        ge.gemm_epilogue(A.view(-1)[1:4097].view(64, 64), B)       # 2-byte offset base: TMA needs 16 B
+    assert e.value.status == ge.Status.MISALIGNED
+    with pytest.raises(ge.GEError) as e:
+        ge.gemm_epilogue(A, B, out=A)                              # C aliases A
+    assert e.value.status == ge.Status.ALIASING
+
+
+def test_host_entry_point():
+    """gemm_epilogue_host (host buffers, copies inside the call) equals the device-pointer path."""
+    prob = workloads.make_problem(300, 264, 200, seed=40, bias_mode="row")
+    Ah = prob.A.pin_memory()
+    Bh = prob.B.t().contiguous().pin_memory().t()
+    Ch = ge.gemm_epilogue_host(Ah, Bh, prob.bias.pin_memory())
+    Cd = ge.gemm_epilogue(Ah.cuda(), Bh.t().contiguous().cuda().t(), prob.bias.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(Ch, Cd.cpu())
