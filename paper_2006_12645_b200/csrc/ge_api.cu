@@ -173,23 +173,35 @@ struct Plan {
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Relative tensor-pipe efficiency of each kernel configuration on large shapes, measured on
+// B200 (profiles/r01_probe.txt: 8192^3, all layouts).  N = 128/64 tiles are shared-memory
+// bandwidth bound (operand bytes per MMA flop double), the CTA pair halves per-SM B traffic.
+double config_eff(int bn, int cg) {
+    if (cg == 2) return bn == 256 ? 1.00 : 0.58;
+    return bn == 256 ? 0.92 : bn == 128 ? 0.52 : 0.30;
+}
+
+// Cost model: per-SM time ~ waves x (tile area per SM) / eff,
+// with waves = ceil(#tiles / #concurrent tiles).  Small problems pick narrow tiles to fill the
+// 148 SMs; large ones the 256 x 256 CTA-pair tile.
 Plan make_plan(const Args& a, int sms) {
-    Plan p{};
-    int cg = a.o.cta_group;
-    int bn = a.o.tile_n;
-    auto tiles = [&](int bn_, int cg_) { return a.batch * cdiv(a.M, 128 * cg_) * cdiv(a.N, bn_); };
-    if (cg == 0) cg = 1;          // heuristic refined by measurement
-    if (bn == 0) {
-        bn = 256;
-        // narrow the N tile while the grid would leave most SMs idle (skinny / small problems)
-        while (bn > (cg == 2 ? 128 : 64) && tiles(bn, cg) * cg < sms) bn /= 2;
-        if (cg == 2 && bn < 128) bn = 128;
+    Plan best{};
+    double best_cost = 0;
+    const int cands[5][2] = {{256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
+    for (const auto& c : cands) {
+        const int bn = c[0], cg = c[1];
+        if (a.o.tile_n && a.o.tile_n != bn) continue;
+        if (a.o.cta_group && a.o.cta_group != cg) continue;
+        const int64_t tiles = a.batch * cdiv(a.M, 128 * cg) * cdiv(a.N, bn);
+        const int64_t conc = std::max(1, sms / cg);
+        const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
+        const double cost = waves * (128.0 * bn) / config_eff(bn, cg);
+        if (best.bn == 0 || cost < best_cost - 1e-9) {
+            best = Plan{bn, cg, ge::stages_for(bn, cg), tiles};
+            best_cost = cost;
+        }
     }
-    p.bn = bn;
-    p.cg = cg;
-    p.tiles = tiles(bn, cg);
-    p.stages = ge::stages_for(bn, cg);
-    return p;
+    return best;
 }
 
 // ------------------------------------------------------------------ tensor maps

@@ -137,9 +137,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < S; ++s) {
-            // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier,
-            // and both producers arrive there.
-            ptx::mbar_init(&full_bar[s], (CG == 2 && !PRO) ? 2 : 1);
+            // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier and
+            // only the leader's producer arrives (expecting both CTAs' bytes).
+            ptx::mbar_init(&full_bar[s], 1);
             ptx::mbar_init(&empty_bar[s], 1);
             ptx::mbar_init(&xform_bar[s], kXformWarps * CG);
         }
@@ -175,8 +175,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     uint8_t* sa = smem_a + s * C_::kAStage;
                     uint8_t* sb = smem_b + s * C_::kBStage;
                     if constexpr (CG == 2 && !PRO) {
+                        // The peer's bytes can only land after the leader's barrier entered this
+                        // phase (the peer first waits on its empty[s], released by the MMA that
+                        // consumed the previous phase), so a transiently negative tx-count is safe.
                         if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * C_::kStageBytes);
-                        else ptx::mbar_arrive_cluster(&full_bar[s], 0);
                         if constexpr (A_MN) {
 #pragma unroll
                             for (int i = 0; i < kRowsPerCta / 64; ++i)
@@ -464,6 +466,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     }
 
     // ---- teardown: every role done; the allocating warp frees TMEM
+    __syncwarp();
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2) {

@@ -68,12 +68,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Arrive on the barrier at the same smem offset in CTA `cta` of the cluster.
+// Arrive on the barrier at the same smem offset in CTA `cta` of the cluster.  Default
+// semantics (release, CTA scope): an explicit .release.cluster compiles to MEMBAR.ALL.GPU,
+// which waits for this thread's outstanding bulk copies.  Cross-CTA ordering of TMEM reads
+// and smem writes is carried by the tcgen05 / proxy fences issued before the arrive.
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
     asm volatile(
         "{\n\t.reg .b32 ra;\n\t"
         "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}"
         ::"r"(smem_u32(bar)), "r"(cta)
         : "memory");
 }
@@ -91,7 +94,7 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 }
 
 __device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ TMA

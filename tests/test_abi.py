@@ -145,9 +145,11 @@ def test_plan_tiles(ge):
     assert p["tile_m"] == 256 and p["num_tiles"] == 32 * 32
     p = ge.plan(35, 8457, 2560)                        # skinny: heuristic narrows the N tile to fill the SMs
     assert p["tile_n"] == 64 and p["num_tiles"] == 133
-    p = ge.plan(2048, 2048, 2048, batch=64)
-    assert p["num_tiles"] >= 64 * 16 * 8
+    p = ge.plan(2048, 2048, 2048, batch=64)           # large: the 256 x 256 CTA-pair tile
+    assert p["cta_group"] == 2 and p["tile_n"] == 256 and p["num_tiles"] == 64 * 8 * 8
     assert p["stages"] >= 4
+    p = ge.plan(8192, 8192, 8192)
+    assert (p["cta_group"], p["tile_n"]) == (2, 256)
 
 
 def test_no_device_fails_loudly(ge):

@@ -22,6 +22,8 @@ ge = pytest.importorskip("paper_2006_12645_b200")
 def dev_operands(prob: workloads.Problem, layouts: str, lda=None, ldb=None):
     """Logical views on the GPU whose storage follows the layout pair (row/col major, padded ld)."""
     def put(logical, lay, ld):
+        if ld is None:      # TMA needs 16-byte row pitch: pad the leading dimension to 8 elements
+            ld = (logical.shape[1 if lay == "r" else 0] + 7) // 8 * 8
         st, ld = workloads.store(logical, lay, ld)
         d = st.cuda()
         R, C = logical.shape
@@ -182,8 +184,9 @@ def test_deterministic():
 def test_errors_raise():
     A = torch.zeros((64, 64), dtype=torch.float16, device="cuda")
     B = torch.zeros((64, 64), dtype=torch.float16, device="cuda")
+    buf = torch.zeros(64 * 64 + 1, dtype=torch.float16, device="cuda")
     with pytest.raises(ge.GEError) as e:
-        ge.gemm_epilogue(A.view(-1)[1:4097].view(64, 64), B)       # 2-byte offset base: TMA needs 16 B
+        ge.gemm_epilogue(buf[1:].view(64, 64), B)                  # 2-byte offset base: TMA needs 16 B
     assert e.value.status == ge.Status.MISALIGNED
     with pytest.raises(ge.GEError) as e:
         ge.gemm_epilogue(A, B, out=A)                              # C aliases A
