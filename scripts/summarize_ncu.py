@@ -1,0 +1,91 @@
+"""Summarise ncu outputs into profiles/ (committed evidence).
+
+usage: summarize_ncu.py --round N --launches gpurun_out/launches.csv --full gpurun_out/prof.ncu-rep
+                        --workload square8192 [--flop F] [--algo-bytes B]
+
+Writes profiles/rNN_launches.csv (the launch list), profiles/rNN_ncu_<workload>.txt (key metrics
+of the --set full capture) and merges per-launch DRAM traffic into profiles/ncu_summary.json,
+which bench.py reads for roofline.traffic."""
+import argparse
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sectors_srcunit_tex_op_read.sum", "sm__cycles_elapsed.avg.per_second", "sm__cycles_active.avg",
+        "launch__grid_size", "launch__cluster_dim_x", "launch__registers_per_thread",
+        "launch__shared_mem_per_block_dynamic", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        res.append({h: (v, u) for h, v, u in zip(hdr, r, units)})
+    return res
+
+
+def to_bytes(v, u):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
+    return float(v.replace(",", "")) * scale
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--round", type=int, required=True)
+    ap.add_argument("--launches")
+    ap.add_argument("--full")
+    ap.add_argument("--workload", default="square8192")
+    ap.add_argument("--flop", type=float, default=2.0 * 8192 ** 3)
+    ap.add_argument("--algo-bytes", type=float, default=2.0 * (8192 * 8192 * 3) + 2 * 8192)
+    a = ap.parse_args()
+    prof = os.path.join(ROOT, "profiles")
+    os.makedirs(prof, exist_ok=True)
+    tag = f"r{a.round:02d}"
+    if a.launches:
+        shutil.copy(a.launches, os.path.join(prof, f"{tag}_launches_{a.workload}.csv"))
+        rows = [r for r in csv.reader(open(a.launches)) if len(r) > 14 and r[12] == "gpu__time_duration.sum"]
+        first = next((i for i, r in enumerate(rows) if "ge_fused_kernel" in r[4]), 0)
+        rows = rows[first:]          # the timed steps; input generation before them is setup
+        tot = sum(float(r[14]) for r in rows)
+        ours = [float(r[14]) for r in rows if "ge_fused_kernel" in r[4]]
+        share = sum(ours) / tot if tot else 0
+        with open(os.path.join(prof, f"{tag}_launches_{a.workload}_summary.txt"), "w") as f:
+            f.write(f"launches: {len(rows)} total, {len(ours)} ge_fused_kernel\n")
+            f.write(f"ge_fused_kernel share of device time from its first launch on (warm-up + steps): {share:.4f}\n")
+            if ours:
+                f.write(f"ge_fused_kernel per-launch ns (cold, serialised): min {min(ours):.0f} "
+                        f"mean {sum(ours)/len(ours):.0f} max {max(ours):.0f}\n")
+    if a.full:
+        recs = [r for r in raw(a.full) if "ge_fused_kernel" in r.get("Kernel Name", ("", ""))[0]]
+        r = recs[-1]
+        lines = [f"kernel: {r['Kernel Name'][0]}"]
+        for k in KEYS:
+            if k in r:
+                lines.append(f"{k:70s} {r[k][0]:>16s} {r[k][1]}")
+        rd = to_bytes(*r["dram__bytes_read.sum"])
+        wr = to_bytes(*r["dram__bytes_write.sum"])
+        t_ns = float(r["gpu__time_duration.sum"][0].replace(",", "")) * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}[
+            r["gpu__time_duration.sum"][1]]
+        lines.append(f"derived: dram traffic per launch {rd + wr:.4g} B vs algorithmic {a.algo_bytes:.4g} B "
+                     f"(x{(rd + wr) / a.algo_bytes:.2f}); TFLOP/s under ncu {a.flop / t_ns / 1e3:.1f}")
+        with open(os.path.join(prof, f"{tag}_ncu_{a.workload}.txt"), "w") as f:
+            f.write("\n".join(lines) + "\n")
+        sp = os.path.join(prof, "ncu_summary.json")
+        d = json.load(open(sp)) if os.path.exists(sp) else {"kernels": {}}
+        d["kernels"][a.workload] = {"dram_bytes_read": rd, "dram_bytes_write": wr, "duration_ns": t_ns,
+                                    "source": f"profiles/{tag}_ncu_{a.workload}.txt (ncu --set full, 1 launch)"}
+        json.dump(d, open(sp, "w"), indent=1)
+        print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
