@@ -83,7 +83,7 @@ typedef struct {
     int32_t prologue;               /* ge_prologue_op */
     const float* prologue_scale;    /* SCALE_K only: device pointer (host pointer for *_host), length K */
     int32_t out_dtype;              /* ge_out_dtype */
-    int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128 or 256) */
+    int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128, 256; 512 with cta_group 2) */
     int32_t cta_group;              /* 0 = heuristic; 1 = single-CTA tiles; 2 = CTA-pair tiles */
 } ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0} */
 
@@ -171,6 +171,15 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
 
 /* Number of fused kernels this library has launched in this process (for launch accounting). */
 uint64_t ge_launch_count(void);
+
+/*
+ * Diagnostics: when the process runs with GE_DEBUG_STATS=1, every launch records per-CTA
+ * counters (16 x uint64 per CTA: total cycles, producer cycles blocked on free stages, MMA
+ * cycles blocked on loaded stages, MMA cycles blocked on a drained accumulator, epilogue
+ * cycles blocked on a full accumulator, epilogue phase timings, reserved).  Copies the last launch's counters of up to
+ * max_ctas CTAs into out (synchronizing) and returns how many were copied (0 when disabled).
+ */
+int32_t ge_debug_read(uint64_t* out, int32_t max_ctas);
 
 /* Library version string. */
 const char* ge_version(void);

@@ -90,6 +90,8 @@ def load_library():
                             ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64)]
     lib.ge_launch_count.restype = ctypes.c_uint64
     lib.ge_launch_count.argtypes = []
+    lib.ge_debug_read.restype = I32
+    lib.ge_debug_read.argtypes = [P, I32]
     lib.ge_version.restype = ctypes.c_char_p
     lib.ge_version.argtypes = []
     _lib = lib
@@ -262,6 +264,17 @@ def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: i
 
 def launch_count() -> int:
     return int(load_library().ge_launch_count())
+
+
+def debug_stats(max_ctas: int = 148):
+    """Per-CTA blocked-cycle counters of the last launch (needs GE_DEBUG_STATS=1), as a list of
+    dicts, or [] when diagnostics are off.  Synchronizes."""
+    import numpy as np
+    buf = np.zeros((max_ctas, 16), dtype=np.uint64)
+    n = load_library().ge_debug_read(buf.ctypes.data, max_ctas)
+    keys = ("total", "prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0",
+            "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math")
+    return [dict(zip(keys, (int(x) for x in buf[i, :10]))) for i in range(n)]
 
 
 def version() -> str:

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -106,10 +107,11 @@ ge_status validate(Args& a) {
     if (o.bias_mode < GE_BIAS_ROW || o.bias_mode > GE_BIAS_FULL) return fail(GE_ERR_INVALID_VALUE, "bad bias_mode");
     if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_RELU) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
     if (o.out_dtype != GE_OUT_F16 && o.out_dtype != GE_OUT_F32) return fail(GE_ERR_INVALID_VALUE, "bad out_dtype");
-    if (o.tile_n != 0 && o.tile_n != 64 && o.tile_n != 128 && o.tile_n != 256)
-        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128 or 256");
+    if (o.tile_n != 0 && o.tile_n != 64 && o.tile_n != 128 && o.tile_n != 256 && o.tile_n != 512)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 256 or 512");
     if (o.cta_group < 0 || o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
-    if (o.cta_group == 2 && o.tile_n == 64) return fail(GE_ERR_INVALID_VALUE, "cta_group 2 needs tile_n 128 or 256");
+    if (o.cta_group == 2 && o.tile_n == 64) return fail(GE_ERR_INVALID_VALUE, "cta_group 2 needs tile_n >= 128");
+    if (o.cta_group == 1 && o.tile_n == 512) return fail(GE_ERR_INVALID_VALUE, "tile_n 512 needs cta_group 2");
     // packed defaults
     const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
     const int64_t minlda = arow ? a.K : a.M, minldb = brow ? a.N : a.K;
@@ -174,20 +176,23 @@ struct Plan {
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Relative tensor-pipe efficiency of each kernel configuration on large shapes, measured on
-// B200 (profiles/r01_probe.txt: 8192^3, all layouts).  N = 128/64 tiles are shared-memory
-// bandwidth bound (operand bytes per MMA flop double), the CTA pair halves per-SM B traffic.
+// B200 (profiles/: 8192^3, all layouts).  N = 128/64 tiles are shared-memory bandwidth bound
+// (operand bytes per MMA flop double), the CTA pair halves per-SM B traffic, and the 256 x 512
+// pair tile moves the least operand data per flop (L2 and HBM) at the cost of a single,
+// non-double-buffered accumulator (its drain is partly exposed: kExposedK below).
 double config_eff(int bn, int cg) {
-    if (cg == 2) return bn == 256 ? 1.00 : 0.58;
+    if (cg == 2) return bn == 512 ? 1.06 : bn == 256 ? 1.00 : 0.58;
     return bn == 256 ? 0.92 : bn == 128 ? 0.52 : 0.30;
 }
 
-// Cost model: per-SM time ~ waves x (tile area per SM) / eff,
-// with waves = ceil(#tiles / #concurrent tiles).  Small problems pick narrow tiles to fill the
-// 148 SMs; large ones the 256 x 256 CTA-pair tile.
+// Cost model: per-SM time ~ waves x per-SM tile area x
+// (K + exposed epilogue) / eff, waves = ceil(#tiles / #concurrent tiles).  Small problems pick
+// narrow tiles to fill the 148 SMs; large ones the CTA-pair tiles.
 Plan make_plan(const Args& a, int sms) {
+    constexpr double kExposedK = 192.0;      // accumulator drain of a single-buffered tile, in K units
     Plan best{};
     double best_cost = 0;
-    const int cands[5][2] = {{256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
+    const int cands[6][2] = {{512, 2}, {256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
     for (const auto& c : cands) {
         const int bn = c[0], cg = c[1];
         if (a.o.tile_n && a.o.tile_n != bn) continue;
@@ -195,13 +200,44 @@ Plan make_plan(const Args& a, int sms) {
         const int64_t tiles = a.batch * cdiv(a.M, 128 * cg) * cdiv(a.N, bn);
         const int64_t conc = std::max(1, sms / cg);
         const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
-        const double cost = waves * (128.0 * bn) / config_eff(bn, cg);
-        if (best.bn == 0 || cost < best_cost - 1e-9) {
+        const double kk = static_cast<double>(std::max<int64_t>(a.K, 64)) + (bn == 512 ? kExposedK : 0.0);
+        const double cost = waves * (128.0 * bn) * kk / config_eff(bn, cg);
+        if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
             best = Plan{bn, cg, ge::stages_for(bn, cg), tiles};
             best_cost = cost;
         }
     }
     return best;
+}
+
+// Raster group: tiles are walked in groups of `group_m` tile-rows so the tiles in flight share
+// A panels (along n) and B panels (along m) in L2.  GE_GROUP_M overrides (tuning only).
+int group_m_for(const Plan& pl, const Args& a, int sms) {
+    static int env = [] {
+        const char* e = getenv("GE_GROUP_M");
+        return e ? atoi(e) : 0;
+    }();
+    (void)pl; (void)a; (void)sms;
+    if (env > 0) return env;
+    return 16;
+}
+
+// Diagnostics (env GE_DEBUG_STATS=1): a zeroed per-CTA counter buffer handed to the kernel.
+unsigned long long* g_dbg = nullptr;
+int g_dbg_ctas = 0;
+unsigned long long* debug_buffer(int sms) {
+    static const bool on = getenv("GE_DEBUG_STATS") != nullptr;
+    if (!on) return nullptr;
+    if (!g_dbg) {
+        if (cudaMalloc(&g_dbg, sizeof(unsigned long long) * 16 * sms) != cudaSuccess) {
+            cudaGetLastError();
+            g_dbg = nullptr;
+            return nullptr;
+        }
+        g_dbg_ctas = sms;
+    }
+    cudaMemset(g_dbg, 0, sizeof(unsigned long long) * 16 * g_dbg_ctas);
+    return g_dbg;
 }
 
 // ------------------------------------------------------------------ tensor maps
@@ -226,7 +262,8 @@ EncodeTiledFn encode_fn() {
 
 // 3-D map {inner, outer, batch} with 128-B swizzle; OOB elements load as zero, stores clip.
 bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, int64_t inner, int64_t outer,
-              int64_t batch, int64_t ld, int64_t stride, uint32_t box_inner, uint32_t box_outer) {
+              int64_t batch, int64_t ld, int64_t stride, uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)batch};
@@ -236,7 +273,7 @@ bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, i
     cuuint32_t box[3] = {box_inner, box_outer, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -262,7 +299,7 @@ ge_status launch(Args& a, cudaStream_t st) {
         if (!a_mn) ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.K, a.M, a.batch, a.lda, a.sA, 64, 128);
         else ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.M, a.K, a.batch, a.lda, a.sA, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for A");
-        const uint32_t brows = static_cast<uint32_t>(pl.bn / pl.cg);
+        const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg);   // B rows per MMA per CTA
         if (!b_mn) ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.K, a.N, a.batch, a.ldb, a.sB, 64, brows);
         else ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.N, a.K, a.batch, a.ldb, a.sB, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for B");
@@ -271,7 +308,7 @@ ge_status launch(Args& a, cudaStream_t st) {
                        (a.batch == 1 || (a.sC * es) % 16 == 0);
     if (c_tma) {
         if (!encode3d(&maps.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, es, a.C, a.N,
-                      a.M, a.batch, a.ldc, a.sC, f32 ? 32 : 64, 32))
+                      a.M, a.batch, a.ldc, a.sC, 32, 32, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
             return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for C");
     }
 
@@ -283,7 +320,18 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg));
     p.num_n_tiles = static_cast<int>(cdiv(a.N, pl.bn));
     p.num_k_blocks = static_cast<int>(cdiv(a.K, ge::kBK));
-    p.group_m = 16;
+    p.group_m = group_m_for(pl, a, sms);
+    {
+        static int hints[3] = {-1, -1, -1};
+        static std::once_flag once;
+        std::call_once(once, [] {
+            const char* e = getenv("GE_L2_HINTS");     // tuning only: "a,b,c" with 0 normal 1 first 2 last
+            if (e) sscanf(e, "%d,%d,%d", &hints[0], &hints[1], &hints[2]);
+        });
+        p.hint_a = hints[0] >= 0 ? hints[0] : 0;
+        p.hint_b = hints[1] >= 0 ? hints[1] : 0;
+        p.hint_c = hints[2] >= 0 ? hints[2] : 0;
+    }
     p.num_tiles = pl.tiles;
     p.bias = has_bias(a.op) ? static_cast<const __half*>(a.bias) : nullptr;
     p.bias_mode = has_bias(a.op) ? a.o.bias_mode : ge::BIAS_NONE;
@@ -299,6 +347,14 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.ldc = a.ldc;
     p.stride_c = a.sC;
     p.c_tma = c_tma ? 1 : 0;
+    p.c_vec = c_tma ? 1 : 0;                      // same alignment conditions as the TMA store
+
+    p.dbg = debug_buffer(sms);
+    static const int noload = getenv("GE_DEBUG_NOLOAD") ? 1 : 0;   // timing experiment only
+    p.dbg_noload = noload;
+    static const int dflags = getenv("GE_DEBUG_FLAGS") ? atoi(getenv("GE_DEBUG_FLAGS")) : 0;   // experiments only
+    p.dbg_flags = dflags;
+    if (dflags & 4) p.c_tma = 0;                  // experiment: st.global epilogue instead of TMA stores
 
     const int64_t clusters = std::min<int64_t>(pl.tiles, sms / pl.cg);
     const int grid = static_cast<int>(std::max<int64_t>(clusters, 1) * pl.cg);
@@ -309,7 +365,8 @@ ge_status launch(Args& a, cudaStream_t st) {
         else e = ge::launch_cg1_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
     } else {
         if (pl.bn == 128) e = ge::launch_cg2_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else e = ge::launch_cg2_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else if (pl.bn == 256) e = ge::launch_cg2_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg2_bn512(a_mn, b_mn, f32, pro, maps, p, grid, st);
     }
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -341,11 +398,11 @@ Workspace g_ws[64];
 namespace ge {
 int smem_bytes_for(int bn, int cg) {
     if (cg == 1) return bn == 64 ? Cfg<64, 1>::kSmemBytes : bn == 128 ? Cfg<128, 1>::kSmemBytes : Cfg<256, 1>::kSmemBytes;
-    return bn == 128 ? Cfg<128, 2>::kSmemBytes : Cfg<256, 2>::kSmemBytes;
+    return bn == 128 ? Cfg<128, 2>::kSmemBytes : bn == 256 ? Cfg<256, 2>::kSmemBytes : Cfg<512, 2>::kSmemBytes;
 }
 int stages_for(int bn, int cg) {
     if (cg == 1) return bn == 64 ? Cfg<64, 1>::kStages : bn == 128 ? Cfg<128, 1>::kStages : Cfg<256, 1>::kStages;
-    return bn == 128 ? Cfg<128, 2>::kStages : Cfg<256, 2>::kStages;
+    return bn == 128 ? Cfg<128, 2>::kStages : bn == 256 ? Cfg<256, 2>::kStages : Cfg<512, 2>::kStages;
 }
 }  // namespace ge
 
@@ -496,8 +553,8 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0,
                        GE_EPI_NONE, opt);
     if (batch < 0 || M < 0 || N < 0 || K < 0 || num_sms <= 0) return fail(GE_ERR_INVALID_VALUE, "bad plan arguments");
-    if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 256)
-        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128 or 256");
+    if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 256 && a.o.tile_n != 512)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 256 or 512");
     if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
     const Plan p = make_plan(a, num_sms);
     if (tile_m) *tile_m = 128 * p.cg;
@@ -509,6 +566,16 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
 }
 
 uint64_t ge_launch_count(void) { return g_launches.load(); }
+
+int32_t ge_debug_read(uint64_t* out, int32_t max_ctas) {
+    if (!g_dbg || !out) return 0;
+    const int n = std::min(max_ctas, g_dbg_ctas);
+    if (cudaMemcpy(out, g_dbg, sizeof(uint64_t) * 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
 
 const char* ge_version(void) { return "gemm_epilogue-b200 0.1.0 (sm_100a, tcgen05/TMA/TMEM)"; }
 

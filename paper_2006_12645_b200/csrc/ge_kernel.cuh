@@ -36,9 +36,8 @@ constexpr int kBK = 64;                 // K per pipeline stage (64 fp16 = one 1
 constexpr int kUmmaK = 16;              // K per tcgen05.mma for 16-bit inputs
 constexpr int kRowsPerCta = 128;        // accumulator rows per CTA (= TMEM lanes)
 constexpr int kSmemBudget = 232448;     // 227 KB dynamic smem per CTA on sm_100
-constexpr int kEpiWarps = 4;
 constexpr int kXformWarps = 4;
-constexpr int kStagingBytes = kEpiWarps * 2 * 32 * 128;   // 2 x (32 rows x 128 B) per epilogue warp
+constexpr int kStagingSetBytes = 16384; // one staging buffer per epilogue warp: 8 x 2 KB (fp16) or 4 x 4 KB (fp32)
 
 enum : int { BIAS_NONE = -1, BIAS_ROW = 0, BIAS_COL = 1, BIAS_FULL = 2 };
 enum : int { PRO_NONE = 0, PRO_SCALE_K = 1, PRO_RELU = 2 };
@@ -61,24 +60,48 @@ struct Params {
     // output
     void* C;
     long long ldc, stride_c;
-    int c_tma;                      // 1: TMA store; 0: st.global fallback
+    int c_tma;                      // 1: TMA store; 0: st.global path
+    int c_vec;                      // st.global path may use 16-B vector stores (aligned rows)
+    // L2 eviction priority of the operand loads / output stores (0 normal, 1 first, 2 last)
+    int hint_a, hint_b, hint_c;
+    // diagnostics (GE_DEBUG_STATS): per-CTA blocked-cycle counters, or nullptr
+    unsigned long long* dbg;
+    int dbg_noload;                 // dev experiment only: stop issuing TMA after the ring is full once
+    int dbg_flags;                  // dev experiments only (GE_DEBUG_FLAGS): 1 skip epilogue, 2 half-major MMA order
 };
+
+// Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
+enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
+             DBG_EPI_REL0 = 5, DBG_EPI_REL1 = 6, DBG_EPI_TILE = 7, DBG_EPI_TMEMLD = 8,
+             DBG_EPI_MATH = 9, DBG_SLOTS = 16 };
 
 template <int BN, int CG>
 struct Cfg {
     static constexpr int kTileM = kRowsPerCta * CG;
-    static constexpr int kBRows = BN / CG;                        // B rows (N) staged per CTA
-    static constexpr int kAStage = kRowsPerCta * kBK * 2;         // 16 KB
+    static constexpr int kUmmaN = BN < 256 ? BN : 256;                // N of one tcgen05.mma
+    static constexpr int kNHalves = BN / kUmmaN;                      // MMAs per K step (BN = 512: 2)
+    static constexpr int kBBlockRows = kUmmaN / CG;                   // B rows per CTA per MMA
+    static constexpr int kBBlockBytes = kBBlockRows * kBK * 2;
+    static constexpr int kBRows = BN / CG;                            // B rows (N) staged per CTA
+    static constexpr int kAStage = kRowsPerCta * kBK * 2;             // 16 KB
     static constexpr int kBStage = kBRows * kBK * 2;
     static constexpr int kStageBytes = kAStage + kBStage;
-    static constexpr int kBarBytes = 1024;
-    static constexpr int kStagesRaw = (kSmemBudget - 1024 - kStagingBytes - kBarBytes) / kStageBytes;
+    static constexpr int kBarBytes = 256;                             // (3S + 6) mbarriers + TMEM slot
+    // Epilogue staging buffers per warp (double-buffered TMA stores).
+    static constexpr int kStagingBufs = 2;
+    static constexpr int kStagingBytes = kStagingBufs * kStagingSetBytes;
+    static constexpr int kBiasBytes = BN * 2;                         // tile's ROW-bias slice (fp16)
+    static constexpr int kStagesRaw = (kSmemBudget - 1024 - kStagingBytes - kBiasBytes - kBarBytes) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStagingBytes + kBarBytes;
-    static constexpr int kTmemCols = 2 * BN;                       // double-buffered fp32 accumulator
+    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStagingBytes + kBiasBytes + kBarBytes;
+    // fp32 accumulator in TMEM: double-buffered when two fit in the 512 columns, else one buffer
+    // drained half by half (per-half barriers let the next tile's first MMAs start early).
+    static constexpr int kAccStages = 2 * BN <= 512 ? 2 : 1;
+    static constexpr int kTmemCols = kAccStages * BN;
     static_assert(kStages >= 2, "not enough smem for a pipeline");
+    static_assert(kBarBytes >= (3 * 8 + 6) * 8 + 4, "barrier area");
     static_assert(kSmemBytes <= kSmemBudget, "smem overflow");
-    static_assert(BN == 64 || BN == 128 || BN == 256, "BN");
+    static_assert(BN == 64 || BN == 128 || BN == 256 || (BN == 512 && CG == 2), "BN");
 };
 
 __device__ __forceinline__ void decode_tile(const Params& p, long long t, int tile_m, int& b, int& mt, int& nt) {
@@ -101,29 +124,42 @@ __device__ __forceinline__ float epi(float acc, float beta, int relu) {
     return relu ? (v > 0.0f ? v : 0.0f) : v;
 }
 
+// Epilogue warps: 8 (two per TMEM lane quarter) for the fp16 fast path, 4 when the fp32 staging
+// or the prologue transform warps need the room.  Non-epilogue warps: 0 TMA, 1 MMA, 2 TMEM, 3 idle.
+__host__ __device__ constexpr int epi_warps(bool out_f32, bool pro) { return (out_f32 || pro) ? 4 : 8; }
+__host__ __device__ constexpr int kernel_threads(bool out_f32, bool pro) {
+    return 32 * (4 + epi_warps(out_f32, pro) + (pro ? kXformWarps : 0));
+}
+
 template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG>
-__global__ void __launch_bounds__(PRO ? 384 : 256, 1)
+__global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO), 1)
 ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const Params p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     using C_ = Cfg<BN, CG>;
     constexpr int S = C_::kStages;
-    constexpr int W = OUT_F32 ? 32 : 64;                 // output columns per epilogue chunk (128 B rows)
+    constexpr int W = 32;                                // output columns per epilogue chunk (one tcgen05.ld)
     constexpr int NCHUNK = BN / W;
-    constexpr uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, BN, A_MN, B_MN);
+    constexpr int EPI_WARPS = epi_warps(OUT_F32, PRO);
+    constexpr int NH = C_::kNHalves;
+    constexpr int HALF_COLS = BN / NH;
+    constexpr uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, C_::kUmmaN, A_MN, B_MN);
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment for the 128-B swizzle atoms, by pointer arithmetic on the __shared__ array so
+    // the compiler keeps the shared address space (LDS/STS instead of generic LD/ST)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + S * C_::kAStage;
     uint8_t* smem_c = smem_b + S * C_::kBStage;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_c + kStagingBytes);
+    __half* smem_bias = reinterpret_cast<__half*>(smem_c + C_::kStagingBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_c + C_::kStagingBytes + C_::kBiasBytes);
     uint64_t* full_bar = bars;                  // [S] TMA -> MMA (or -> transform)
     uint64_t* empty_bar = bars + S;             // [S] MMA -> TMA
     uint64_t* xform_bar = bars + 2 * S;         // [S] transform -> MMA (PRO only)
-    uint64_t* tfull_bar = bars + 3 * S;         // [2] MMA -> epilogue
-    uint64_t* tempty_bar = bars + 3 * S + 2;    // [2] epilogue -> MMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+    uint64_t* tfull_bar = bars + 3 * S;         // [acc] MMA -> epilogue
+    uint64_t* tempty_bar = bars + 3 * S + 2;    // [acc * NH + half] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 6);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -143,10 +179,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             ptx::mbar_init(&empty_bar[s], 1);
             ptx::mbar_init(&xform_bar[s], kXformWarps * CG);
         }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(&tfull_bar[b], 1);
-            ptx::mbar_init(&tempty_bar[b], kEpiWarps * CG);
-        }
+        for (int b = 0; b < 2; ++b) ptx::mbar_init(&tfull_bar[b], 1);
+        for (int b = 0; b < 4; ++b) ptx::mbar_init(&tempty_bar[b], EPI_WARPS * CG);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
@@ -155,6 +189,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    unsigned long long* dbg = p.dbg ? p.dbg + blockIdx.x * DBG_SLOTS : nullptr;
+    const long long t_start = clock64();
     const int cluster_id = blockIdx.x / CG;
     const int num_clusters = gridDim.x / CG;
     const int nkb = p.num_k_blocks;
@@ -164,50 +200,52 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         if (lane == 0) {
             int s = 0;
             uint32_t phase = 0;
+            const uint64_t pol_a = ptx::l2_policy(p.hint_a);
+            const uint64_t pol_b = ptx::l2_policy(p.hint_b);
             for (long long t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int b, mt, nt;
                 decode_tile(p, t, C_::kTileM, b, mt, nt);
                 const int m0 = mt * C_::kTileM + rank * kRowsPerCta;
-                const int n0 = nt * BN + rank * C_::kBRows;
+                const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
                 for (int kb = 0; kb < nkb; ++kb) {
-                    ptx::mbar_wait(&empty_bar[s], phase ^ 1);
+                    ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg ? &dbg[DBG_PROD_EMPTY] : nullptr);
                     const int k0 = kb * kBK;
                     uint8_t* sa = smem_a + s * C_::kAStage;
                     uint8_t* sb = smem_b + s * C_::kBStage;
+                    if (p.dbg_noload && (t != cluster_id || kb >= S)) {
+                        // timing experiment (GE_DEBUG_NOLOAD): operands stay resident, results invalid
+                        if (CG == 1 || PRO || leader) ptx::mbar_arrive(&full_bar[s]);
+                        if (++s == S) { s = 0; phase ^= 1; }
+                        continue;
+                    }
                     if constexpr (CG == 2 && !PRO) {
                         // The peer's bytes can only land after the leader's barrier entered this
                         // phase (the peer first waits on its empty[s], released by the MMA that
                         // consumed the previous phase), so a transiently negative tx-count is safe.
                         if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * C_::kStageBytes);
-                        if constexpr (A_MN) {
-#pragma unroll
-                            for (int i = 0; i < kRowsPerCta / 64; ++i)
-                                ptx::tma_load_3d_pair(sa + i * 8192, &tmap_a, &full_bar[s], m0 + i * 64, k0, b);
-                        } else {
-                            ptx::tma_load_3d_pair(sa, &tmap_a, &full_bar[s], k0, m0, b);
-                        }
-                        if constexpr (B_MN) {
-#pragma unroll
-                            for (int i = 0; i < C_::kBRows / 64; ++i)
-                                ptx::tma_load_3d_pair(sb + i * 8192, &tmap_b, &full_bar[s], n0 + i * 64, k0, b);
-                        } else {
-                            ptx::tma_load_3d_pair(sb, &tmap_b, &full_bar[s], k0, n0, b);
-                        }
                     } else {
                         ptx::mbar_arrive_expect_tx(&full_bar[s], C_::kStageBytes);
-                        if constexpr (A_MN) {
+                    }
+                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
+                        if constexpr (CG == 2 && !PRO) ptx::tma_load_3d_pair(dst, map, &full_bar[s], c0, c1, b, pol);
+                        else ptx::tma_load_3d(dst, map, &full_bar[s], c0, c1, b, pol);
+                    };
+                    if constexpr (A_MN) {
 #pragma unroll
-                            for (int i = 0; i < kRowsPerCta / 64; ++i)
-                                ptx::tma_load_3d(sa + i * 8192, &tmap_a, &full_bar[s], m0 + i * 64, k0, b);
-                        } else {
-                            ptx::tma_load_3d(sa, &tmap_a, &full_bar[s], k0, m0, b);
-                        }
+                        for (int i = 0; i < kRowsPerCta / 64; ++i) load(sa + i * 8192, &tmap_a, m0 + i * 64, k0, pol_a);
+                    } else {
+                        load(sa, &tmap_a, k0, m0, pol_a);
+                    }
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        uint8_t* sbh = sb + h * C_::kBBlockBytes;
+                        const int nh = n0 + h * C_::kUmmaN;
                         if constexpr (B_MN) {
 #pragma unroll
-                            for (int i = 0; i < C_::kBRows / 64; ++i)
-                                ptx::tma_load_3d(sb + i * 8192, &tmap_b, &full_bar[s], n0 + i * 64, k0, b);
+                            for (int i = 0; i < C_::kBBlockRows / 64; ++i)
+                                load(sbh + i * 8192, &tmap_b, nh + i * 64, k0, pol_b);
                         } else {
-                            ptx::tma_load_3d(sb, &tmap_b, &full_bar[s], k0, n0, b);
+                            load(sbh, &tmap_b, k0, nh, pol_b);
                         }
                     }
                     if (++s == S) { s = 0; phase ^= 1; }
@@ -216,115 +254,162 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA, one thread) =====================
-        if (leader && lane == 0 && nkb > 0) {
-            int s = 0;
-            uint32_t phase = 0;
-            int it = 0;
+        if (leader && nkb > 0) {
+            // The whole warp runs this loop converged (warp-uniform state, so the descriptors live
+            // in uniform registers); one elected lane issues each tcgen05 instruction.  The tensor
+            // pipe queues only about one MMA, so the code between consecutive MMAs (barrier wait,
+            // fence, commit) is kept minimal: it shows up directly as tensor idle time.
+            uint64_t* const ready = PRO ? xform_bar : full_bar;
             const uint32_t a_base = ptx::smem_u32(smem_a);
             const uint32_t b_base = ptx::smem_u32(smem_b);
+            int s = 0, it = 0;
+            uint32_t phase = 0;
             for (long long t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
-                const int acc = it & 1;
-                const uint32_t acc_phase = (it >> 1) & 1;
-                ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-                ptx::tc_fence_after();
+                const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
+                const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kb = 0; kb < nkb; ++kb) {
-                    ptx::mbar_wait(PRO ? &xform_bar[s] : &full_bar[s], phase);
+                    ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
                     ptx::tc_fence_after();
                     const uint32_t sa = a_base + s * C_::kAStage;
                     const uint32_t sb = b_base + s * C_::kBStage;
-#pragma unroll
-                    for (int k = 0; k < kBK / kUmmaK; ++k) {
-                        // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
-                        // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
-                        // SBO = next 8-row K group (1024 B).
+                    // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
+                    // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
+                    // SBO = next 8-row K group (1024 B).
+                    auto mma_one = [&](int h, int k) {
+                        const uint32_t sbh = sb + h * C_::kBBlockBytes;
                         const uint64_t ad = A_MN ? ptx::make_sw128_desc(sa + k * 2048, 8192, 1024)
                                                  : ptx::make_sw128_desc(sa + k * 32, 0, 1024);
-                        const uint64_t bd = B_MN ? ptx::make_sw128_desc(sb + k * 2048, 8192, 1024)
-                                                 : ptx::make_sw128_desc(sb + k * 32, 0, 1024);
-                        ptx::mma_f16<CG>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+                        const uint64_t bd = B_MN ? ptx::make_sw128_desc(sbh + k * 2048, 8192, 1024)
+                                                 : ptx::make_sw128_desc(sbh + k * 32, 0, 1024);
+                        ptx::mma_f16_elect<CG>(d_tmem + h * C_::kUmmaN, ad, bd, IDESC, (kb | k) != 0);
+                    };
+                    if (kb == 0) {
+                        // first k-block of a tile: start on accumulator half 0 as soon as the
+                        // epilogue has drained it, then wait for half 1
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) {
+                            ptx::mbar_wait_timed(&tempty_bar[acc * NH + h], acc_phase ^ 1,
+                                                 (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                            ptx::tc_fence_after();
+#pragma unroll
+                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(h, k);
+                        }
+                    } else if (p.dbg_flags & 2) {
+#pragma unroll
+                        for (int h = 0; h < NH; ++h)
+#pragma unroll
+                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(h, k);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < kBK / kUmmaK; ++k)
+#pragma unroll
+                            for (int h = 0; h < NH; ++h) mma_one(h, k);
                     }
-                    ptx::mma_commit<CG>(&empty_bar[s]);          // smem slot free once these MMAs finish
-                    if (kb == nkb - 1) ptx::mma_commit<CG>(&tfull_bar[acc]);
+                    ptx::mma_commit_elect<CG>(&empty_bar[s]);    // smem slot free once these MMAs finish
+                    if (kb == nkb - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
                     if (++s == S) { s = 0; phase ^= 1; }
                 }
             }
         }
-    } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+    } else if (warp >= 4 && warp < 4 + EPI_WARPS) {
         // ===================== epilogue: TMEM -> regs -> bias/ReLU -> smem -> TMA store ======
+        // EPI_WARPS / 4 column groups: warp e drains TMEM lane quarter (e % 4) for the 32-column
+        // chunks c = h*CPH_ALL + j*NG + e/4 of each accumulator half h.
+        const int e_idx = warp - 4;
         const int q = warp & 3;                                  // TMEM lane quarter of this warp
-        uint8_t* stage_c = smem_c + (warp - 4) * (2 * 32 * 128);
+        const int grp = e_idx / 4;
+        constexpr int NG = EPI_WARPS / 4;
+        constexpr int ES = OUT_F32 ? 4 : 2;
+        constexpr int ROWB = W * ES;                             // staged bytes per row: 64 (fp16) / 128 (fp32)
+        constexpr int STG = 32 * ROWB;                           // one staging buffer (32 rows)
+        constexpr int NV = ROWB / 16;                            // 16-B vectors per row
+        constexpr int NWORD = ROWB / 4;                          // 32-bit words per row
+        constexpr int CPH_ALL = HALF_COLS / W;                   // 32-column chunks per accumulator half
+        constexpr int CPH = CPH_ALL / NG;                        // ... owned by this warp
+        // Single-buffered accumulator (BN = 512), fp16 out: compute all of this warp's chunks of a
+        // half into packed registers first and release the half before any store, so the next
+        // tile's MMAs restart as early as possible.  Otherwise drain chunk by chunk.
+        constexpr bool BATCH = (C_::kAccStages == 1) && !OUT_F32 && NG == 2;
+        constexpr int NBUF = C_::kStagingBufs;
+        uint8_t* stage_c = smem_c + e_idx * (NBUF * STG);
+        const uint64_t pol_c = ptx::l2_policy(p.hint_c);
         int buf = 0;
         int it = 0;
         for (long long t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
             int b, mt, nt;
             decode_tile(p, t, C_::kTileM, b, mt, nt);
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
+            const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
             const int row0 = mt * C_::kTileM + rank * kRowsPerCta + q * 32;   // first row of this warp
             const int row = row0 + lane;
+            const __half* bias_b = p.bias ? p.bias + b * p.stride_bias : nullptr;
+            // Bias operands are fetched while this tile's MMAs still run (global loads would miss
+            // the ~2 KB of L1 the smem carve-out leaves): the ROW slice goes to smem as fp32.
+            float beta_col = 0.0f;
+            if (p.bias_mode == BIAS_COL && row < p.M) beta_col = __half2float(bias_b[row]);
+            if (p.bias_mode == BIAS_ROW) {
+                ptx::named_bar_sync(1, EPI_WARPS * 32);            // previous tile's reads are done
+                for (int i = threadIdx.x - 128; i < BN; i += EPI_WARPS * 32) {
+                    const int col = nt * BN + i;
+                    smem_bias[i] = col < p.N ? bias_b[col] : __float2half_rn(0.0f);
+                }
+                ptx::named_bar_sync(1, EPI_WARPS * 32);
+            }
             if (nkb > 0) {
-                ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+                ptx::mbar_wait_timed(&tfull_bar[acc], acc_phase, (dbg && e_idx == 0 && lane == 0) ? &dbg[DBG_EPI_TFULL] : nullptr);
                 ptx::tc_fence_after();
             }
-            float beta_col = 0.0f;
-            if (p.bias_mode == BIAS_COL && row < p.M)
-                beta_col = __half2float(p.bias[b * p.stride_bias + row]);
-            const __half* bias_b = p.bias ? p.bias + b * p.stride_bias : nullptr;
-#pragma unroll 1
-            for (int c = 0; c < NCHUNK; ++c) {
-                uint32_t v[W];
+            const long long t_epi0 = (dbg && e_idx == 0) ? clock64() : 0;
+            const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+
+            // TMEM columns of chunk c -> registers (zeros when K == 0)
+            auto load = [&](const int c, uint32_t* v) {
                 if (nkb > 0) {
-                    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * W;
-                    ptx::tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-                    if constexpr (W == 64)
-                        ptx::tmem_ld_32x32b_x32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-                    ptx::tmem_ld_wait();
+                    ptx::tmem_ld_32x32b_x32(tm_row + c * W, v);
                 } else {
 #pragma unroll
                     for (int e = 0; e < W; ++e) v[e] = 0u;
                 }
-                if (c == NCHUNK - 1 && nkb > 0) {
-                    // accumulator buffer fully read: hand it back to the MMA warp
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&tempty_bar[acc], 0);
-                        else ptx::mbar_arrive(&tempty_bar[acc]);
-                    }
+            };
+            // hand accumulator half h back to the MMA warp (all of this warp's reads are done)
+            auto release = [&](const int h) {
+                if (nkb == 0) return;
+                if (dbg && e_idx == 0 && lane == 0)
+                    dbg[h == 0 ? DBG_EPI_REL0 : DBG_EPI_REL1] += static_cast<unsigned long long>(clock64() - t_epi0);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&tempty_bar[acc * NH + h], 0);
+                    else ptx::mbar_arrive(&tempty_bar[acc * NH + h]);
                 }
+            };
+            // S2 of Listing 1: v = acc + beta, relu, one RNE conversion; packed into NWORD words
+            auto compute = [&](const int c, const uint32_t* v, uint32_t* w) {
                 const int col0 = nt * BN + c * W;
-                // ---- bias + ReLU in fp32, convert, pack into 8 x 16-B vectors
                 float f[W];
 #pragma unroll
                 for (int e = 0; e < W; ++e) f[e] = __uint_as_float(v[e]);
                 if (p.bias_mode == BIAS_ROW) {
-                    if (p.bias_vec && col0 + W <= p.N) {
+                    const uint4* bs = reinterpret_cast<const uint4*>(smem_bias + c * W);     // broadcast reads
 #pragma unroll
-                        for (int g = 0; g < W / 8; ++g) {
-                            const uint4 hb = __ldg(reinterpret_cast<const uint4*>(bias_b + col0 + g * 8));
-                            const __half2* h2 = reinterpret_cast<const __half2*>(&hb);
+                    for (int g = 0; g < W / 8; ++g) {
+                        const uint4 hb = bs[g];
+                        const __half2* h2 = reinterpret_cast<const __half2*>(&hb);
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float2 bf = __half22float2(h2[e]);
-                                f[g * 8 + 2 * e] = epi(f[g * 8 + 2 * e], bf.x, p.relu);
-                                f[g * 8 + 2 * e + 1] = epi(f[g * 8 + 2 * e + 1], bf.y, p.relu);
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < W; ++e) {
-                            const int col = col0 + e;
-                            const float bv = col < p.N ? __half2float(bias_b[col]) : 0.0f;
-                            f[e] = epi(f[e], bv, p.relu);
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 bf = __half22float2(h2[e]);
+                            f[g * 8 + 2 * e] = epi(f[g * 8 + 2 * e], bf.x, p.relu);
+                            f[g * 8 + 2 * e + 1] = epi(f[g * 8 + 2 * e + 1], bf.y, p.relu);
                         }
                     }
                 } else if (p.bias_mode == BIAS_FULL) {
-                    const __half* brow = bias_b + static_cast<long long>(row) * p.ldbias;
-                    if (p.bias_vec && col0 + W <= p.N && row < p.M) {
+                    const __half* bsrc = bias_b + static_cast<long long>(row) * p.ldbias;
+                    const bool in_row = row < p.M;
+                    if (p.bias_vec && col0 + W <= p.N && in_row) {
 #pragma unroll
                         for (int g = 0; g < W / 8; ++g) {
-                            const uint4 hb = __ldg(reinterpret_cast<const uint4*>(brow + col0 + g * 8));
+                            const uint4 hb = __ldg(reinterpret_cast<const uint4*>(bsrc + col0 + g * 8));
                             const __half2* h2 = reinterpret_cast<const __half2*>(&hb);
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
@@ -337,7 +422,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
                         for (int e = 0; e < W; ++e) {
                             const int col = col0 + e;
-                            const float bv = (col < p.N && row < p.M) ? __half2float(brow[col]) : 0.0f;
+                            const float bv = (col < p.N && in_row) ? __half2float(bsrc[col]) : 0.0f;
                             f[e] = epi(f[e], bv, p.relu);
                         }
                     }
@@ -346,61 +431,108 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
                     for (int e = 0; e < W; ++e) f[e] = epi(f[e], bv, p.relu);
                 }
-                uint4 out[8];
                 if constexpr (OUT_F32) {
 #pragma unroll
-                    for (int g = 0; g < 8; ++g)
-                        out[g] = make_uint4(__float_as_uint(f[4 * g]), __float_as_uint(f[4 * g + 1]),
-                                            __float_as_uint(f[4 * g + 2]), __float_as_uint(f[4 * g + 3]));
+                    for (int e = 0; e < W; ++e) w[e] = __float_as_uint(f[e]);
                 } else {
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        uint32_t w4[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const __half2 h = __floats2half2_rn(f[8 * g + 2 * e], f[8 * g + 2 * e + 1]);
-                            w4[e] = *reinterpret_cast<const uint32_t*>(&h);
-                        }
-                        out[g] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    for (int e = 0; e < W / 2; ++e) {
+                        const __half2 hh = __floats2half2_rn(f[2 * e], f[2 * e + 1]);
+                        w[e] = *reinterpret_cast<const uint32_t*>(&hh);
                     }
                 }
+            };
+            // packed row of chunk c -> C (TMA store through a swizzled staging chunk, or st.global)
+            auto store = [&](const int c, const uint32_t* w) {
+                const int col0 = nt * BN + c * W;
                 if (p.c_tma) {
-                    // ---- swizzled staging chunk (32 rows x 128 B), then one TMA store per warp
-                    if (lane == 0) ptx::bulk_wait_read<1>();        // the store that last used `buf` has read it
+                    // The swizzle matches the C tensor map: 128-B rows use SWIZZLE_128B (16-B chunk
+                    // ^= row % 8), 64-B rows SWIZZLE_64B (chunk ^= (row / 2) % 4); both are
+                    // bank-conflict-free for a warp's 16-B stores.
+                    if (lane == 0) ptx::bulk_wait_read<NBUF - 1>(); // the store that last used `buf` has read it
                     __syncwarp();
-                    uint8_t* sc = stage_c + buf * (32 * 128);
+                    uint8_t* sc = stage_c + buf * STG;
 #pragma unroll
-                    for (int g = 0; g < 8; ++g)
-                        *reinterpret_cast<uint4*>(sc + lane * 128 + ((g ^ (lane & 7)) * 16)) = out[g];
+                    for (int g = 0; g < NV; ++g) {
+                        const int pc = (ROWB == 128) ? (g ^ (lane & 7)) : (g ^ ((lane >> 1) & 3));
+                        *reinterpret_cast<uint4*>(sc + lane * ROWB + pc * 16) =
+                            make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
+                    }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        ptx::tma_store_3d(&tmap_c, sc, col0, row0, b);
+                        ptx::tma_store_3d(&tmap_c, sc, col0, row0, b, pol_c);
                         ptx::bulk_commit();
                     }
-                    buf ^= 1;
+                    buf = (buf + 1 == NBUF) ? 0 : buf + 1;
                 } else if (row < p.M) {
-                    // ---- st.global fallback for a C whose base/ldc breaks the TMA alignment rules
+                    // st.global path: C whose base/ldc breaks the TMA alignment rules (scalar stores),
+                    // or 16-B aligned rows written straight from registers (c_vec)
                     const long long off = static_cast<long long>(b) * p.stride_c + static_cast<long long>(row) * p.ldc;
-                    if constexpr (OUT_F32) {
+                    if (p.c_vec && col0 + W <= p.N) {
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.C) + (off + col0) * ES);
+#pragma unroll
+                        for (int g = 0; g < NV; ++g) dst[g] = make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
+                    } else if constexpr (OUT_F32) {
                         float* crow = reinterpret_cast<float*>(p.C) + off;
 #pragma unroll
                         for (int e = 0; e < W; ++e)
-                            if (col0 + e < p.N) crow[col0 + e] = f[e];
+                            if (col0 + e < p.N) crow[col0 + e] = __uint_as_float(w[e]);
                     } else {
                         __half* crow = reinterpret_cast<__half*>(p.C) + off;
-                        const __half* hv = reinterpret_cast<const __half*>(out);
+                        const __half* hv = reinterpret_cast<const __half*>(w);
 #pragma unroll
                         for (int e = 0; e < W; ++e)
                             if (col0 + e < p.N) crow[col0 + e] = hv[e];
                     }
                 }
+            };
+
+            if (p.dbg_flags & 1) {          // timing experiment: release without draining
+#pragma unroll
+                for (int h = 0; h < NH; ++h) release(h);
+                continue;
             }
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                if constexpr (BATCH) {
+                    uint32_t packed[CPH][NWORD];
+#pragma unroll
+                    for (int j = 0; j < CPH; ++j) {
+                        uint32_t v[W];
+                        const long long tl0 = (dbg && e_idx == 0) ? clock64() : 0;
+                        load(h * CPH_ALL + j * NG + grp, v);
+                        if (nkb > 0) ptx::tmem_ld_wait();
+                        const long long tl1 = (dbg && e_idx == 0) ? clock64() : 0;
+                        if (j == CPH - 1) release(h);
+                        compute(h * CPH_ALL + j * NG + grp, v, packed[j]);
+                        if (dbg && e_idx == 0 && lane == 0) {
+                            dbg[DBG_EPI_TMEMLD] += static_cast<unsigned long long>(tl1 - tl0);
+                            dbg[DBG_EPI_MATH] += static_cast<unsigned long long>(clock64() - tl1);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < CPH; ++j) store(h * CPH_ALL + j * NG + grp, packed[j]);
+                } else {
+#pragma unroll 1
+                    for (int j = 0; j < CPH; ++j) {
+                        const int c = h * CPH_ALL + j * NG + grp;
+                        uint32_t v[W];
+                        load(c, v);
+                        if (nkb > 0) ptx::tmem_ld_wait();
+                        if (j == CPH - 1) release(h);
+                        uint32_t w[NWORD];
+                        compute(c, v, w);
+                        store(c, w);
+                    }
+                }
+            }
+            if (dbg && e_idx == 0 && lane == 0) dbg[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
         }
         if (p.c_tma && lane == 0) ptx::bulk_wait<0>();
-    } else if (PRO && warp >= 4 + kEpiWarps) {
+    } else if (PRO && warp >= 4 + EPI_WARPS) {
         // ===================== prologue transform of the A stage (in place, in smem) ==========
-        const int xt = threadIdx.x - (4 + kEpiWarps) * 32;      // 0..127
+        const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
         int s = 0;
         uint32_t phase = 0;
         for (long long t = cluster_id; t < p.num_tiles; t += num_clusters) {
@@ -467,6 +599,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 
     // ---- teardown: every role done; the allocating warp frees TMEM
     __syncwarp();
+    if (dbg && warp == 1 && lane == 0) {
+        dbg[DBG_TOTAL] = static_cast<unsigned long long>(clock64() - t_start);
+    }
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2) {

@@ -28,7 +28,7 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(PRO ? 384 : 256, 1, 1);
+    cfg.blockDim = dim3(kernel_threads(OUT_F32, PRO), 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -76,5 +76,6 @@ cudaError_t launch_cg1_bn128(bool, bool, bool, bool, const Maps&, const Params&,
 cudaError_t launch_cg1_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn512(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 
 }  // namespace ge

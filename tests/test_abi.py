@@ -32,14 +32,14 @@ def lib(ge):
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(?:ge_status|uint64_t|const char\*)\s+(\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(?:ge_status|uint64_t|int32_t|const char\*)\s+(\w+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(lib):
     names = declared_functions()
     assert {"gemm_epilogue", "gemm_epilogue_batched", "gemm_epilogue_host", "ge_validate", "ge_status_string",
             "ge_last_error_detail", "ge_plan", "ge_launch_count", "ge_version",
-            "ge_release_workspace"} <= set(names)
+            "ge_release_workspace", "ge_debug_read"} <= set(names)
     for n in names:
         assert hasattr(lib, n), n
 
@@ -149,7 +149,9 @@ def test_plan_tiles(ge):
     assert p["cta_group"] == 2 and p["tile_n"] == 256 and p["num_tiles"] == 64 * 8 * 8
     assert p["stages"] >= 4
     p = ge.plan(8192, 8192, 8192)
-    assert (p["cta_group"], p["tile_n"]) == (2, 256)
+    assert p["cta_group"] == 2 and p["tile_n"] in (256, 512)
+    with pytest.raises(ge.GEError):
+        ge.plan(8192, 8192, 8192, tile_n=96)
 
 
 def test_no_device_fails_loudly(ge):

@@ -45,7 +45,7 @@ def exact_expect(out, out_dtype):
     return out if out_dtype == torch.float32 else oracle.f16_decode(oracle.f16_encode(out))
 
 
-CONFIGS = [(64, 1), (128, 1), (256, 1), (128, 2), (256, 2)]
+CONFIGS = [(64, 1), (128, 1), (256, 1), (128, 2), (256, 2), (512, 2)]
 
 
 # ------------------------------------------------------------------ small full-matrix parity
@@ -88,7 +88,7 @@ def test_epilogue_variants(bias_mode, out_dtype, op):
 
 @pytest.mark.parametrize("prologue", ["scale_k", "relu"])
 @pytest.mark.parametrize("layouts", workloads.LAYOUTS)
-@pytest.mark.parametrize("tile_n,cg", [(256, 1), (256, 2), (64, 1)])
+@pytest.mark.parametrize("tile_n,cg", [(256, 1), (256, 2), (64, 1), (512, 2)])
 def test_prologue(prologue, layouts, tile_n, cg):
     """Prologue fusion (Sec. VII-C; SCALE_K = DESIGN.md R-C12): exact on small
     integers with s in {0.5, 1, 2}, within the bound on uniform data."""
