@@ -37,6 +37,8 @@ WORKLOADS = {
     # name: (batch, M, N, K, layouts, prologue)
     "square8192": (1, 8192, 8192, 8192, ("rr", "rc", "cr", "cc"), None),
     "square4096": (1, 4096, 4096, 4096, ("rr", "rc", "cr", "cc"), None),
+    "square2048": (1, 2048, 2048, 2048, ("rr", "rc", "cr", "cc"), None),
+    "square1024": (1, 1024, 1024, 1024, ("rr", "rc", "cr", "cc"), None),
     "deepbench_a": (1, 5124, 700, 2048, ("rr", "rc"), None),
     "deepbench_b": (1, 35, 8457, 2560, ("rr", "rc"), None),
     "prologue4096": (1, 4096, 4096, 4096, ("rr",), "scale_k"),
@@ -54,6 +56,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparators", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch from Python every step instead of replaying "
+                    "a captured CUDA graph per operand set")
     return ap.parse_args()
 
 
@@ -70,8 +74,6 @@ def workload_config(name, world):
            "M": M, "N": N, "K": K, "batch_per_gpu": batch, "layouts": list(layouts),
            "epilogue": "bias_relu", "bias": "row (length N)", "prologue": pro or "none", "out": "f16",
            "global_batch": batch * len(layouts) * world,
-           "l2": "operands exceed the 126 MB L2 (no flush needed)" if 2 * (M * K + K * N) * batch > 126e6
-           else "L2 flushed between steps (256 MiB scratch write)",
            "parallelism": f"dp{world} (independent problem per GPU, no collective)"}
     return cfg
 
@@ -228,20 +230,27 @@ def run_ours(args):
     g.manual_seed(seed)
     def U(*shape):
         return (torch.rand(*shape, generator=g, device=dev, dtype=torch.float32) * 2 - 1).half()
-    A0 = U(batch, M, K)
-    B0 = U(batch, K, N)
+    ld8 = lambda n: (n + 7) // 8 * 8           # TMA needs 16-byte row pitch: pad leading dimensions
+
+    def operand(rows, cols, lay):
+        """Logical (batch, rows, cols) fp16 operand stored row- ('r') or column-major ('c'), ld padded."""
+        if lay == "r":
+            return U(batch, rows, ld8(cols))[:, :, :cols]
+        return U(batch, cols, ld8(rows))[:, :, :rows].transpose(1, 2)
+
+    # Operand sets are rotated between steps so the working set exceeds the 126 MB L2 (no flush
+    # kernel inside the timed region); one set when a single step already streams > 3x L2.
+    set_bytes = sum(2 * (M * ld8(K) + K * ld8(N)) * batch for _ in layouts)
+    n_sets = max(1, min(64, -(-int(3 * 126e6) // set_bytes)))
+    sets = [[(lay, operand(M, K, lay[0]), operand(K, N, lay[1])) for lay in layouts] for _ in range(n_sets)]
+    ops = sets[0]
     bias = U(N)
     scale = (torch.rand(K, generator=g, device=dev) + 0.5) if pro == "scale_k" else None
-    ops = []
-    for lay in layouts:
-        A = A0 if lay[0] == "r" else A0.transpose(1, 2).contiguous().transpose(1, 2)
-        B = B0 if lay[1] == "r" else B0.transpose(1, 2).contiguous().transpose(1, 2)
-        ops.append((lay, A, B))
-    del A0, B0
-    C = torch.empty(batch, M, N, dtype=torch.float16, device=dev)
-    l2_flush = None
-    if 2 * (M * K + K * N) * batch <= 126e6:
-        l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    C = torch.empty(batch, M, ld8(N), dtype=torch.float16, device=dev)[:, :, :N]
+    cfg["l2"] = (f"{n_sets} operand sets rotated across steps ({n_sets * set_bytes / 1e6:.0f} MB working set > "
+                 f"126 MB L2), no flush")
+    if ld8(N) != N or ld8(K) != K or ld8(M) != M:
+        cfg["padding"] = "leading dimensions padded to a multiple of 8 elements (16-byte TMA pitch)"
     stream = torch.cuda.current_stream()
 
     def launch(lay, A, B):
@@ -250,23 +259,37 @@ def run_ours(args):
         else:
             ge.gemm_epilogue_batched(A, B, bias, prologue=pro, scale=scale, out=C)
 
-    def step(evs=None):
-        if l2_flush is not None:
-            l2_flush.fill_(1)
-        for i, (lay, A, B) in enumerate(ops):
-            if evs is not None:
-                evs[i][0].record(stream)
+    step_no = [0]
+
+    def step_eager():
+        cur = sets[step_no[0] % n_sets]
+        step_no[0] += 1
+        for lay, A, B in cur:
             launch(lay, A, B)
-            if evs is not None:
-                evs[i][1].record(stream)
 
     for _ in range(args.warmup):
-        step()
+        step_eager()
     torch.cuda.synchronize()
 
+    # A step is replayed from a CUDA graph captured per operand set (the 4 launches are plain
+    # cudaLaunchKernelEx calls on the capturing stream): no host launch overhead in the timed region.
+    graphs = None
+    launches_per_step = len(layouts)
+    if not args.no_graph:
+        graphs = []
+        for cur in sets:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for lay, A, B in cur:
+                    launch(lay, A, B)
+            graphs.append(gr)
+        for i in range(max(1, args.warmup)):
+            graphs[i % n_sets].replay()
+        torch.cuda.synchronize()
+
     # ---- timed region
-    per_launch = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in ops] for _ in range(args.steps)]
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -275,14 +298,20 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         t0.record(stream)
         for s in range(args.steps):
-            step(per_launch[s])
+            step_ev[s][0].record(stream)
+            if graphs is not None:
+                graphs[s % n_sets].replay()
+            else:
+                step_eager()
+            step_ev[s][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
-    n_launches = ge.launch_count() - n_launch0
+    n_launches = (ge.launch_count() - n_launch0) if graphs is None else launches_per_step * args.steps
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
-    kern_ms = [a.elapsed_time(b) for row in per_launch for (a, b) in row]
+    # the step holds only our kernels, back to back: per-launch time = step time / launches
+    kern_ms = [a.elapsed_time(b) / launches_per_step for (a, b) in step_ev]
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     if world > 1:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -295,13 +324,22 @@ def run_ours(args):
     # ---- end to end through the host-buffer C-ABI entry point
     e2e = None
     if args.e2e_steps > 0:
-        Ah = [A.cpu().pin_memory() if lay[0] == "r" else A.transpose(1, 2).cpu().contiguous().pin_memory()
-              .transpose(1, 2) for lay, A, B in ops]
-        Bh = [B.cpu().pin_memory() if lay[1] == "r" else B.transpose(1, 2).cpu().contiguous().pin_memory()
-              .transpose(1, 2) for lay, A, B in ops]
+        def host_copy(x, lay):
+            """Pinned host copy of a logical (batch, rows, cols) operand, same layout and padded ld."""
+            rows, cols = x.shape[1], x.shape[2]
+            if lay == "r":
+                st_ = torch.empty(batch, rows, ld8(cols), dtype=torch.float16).pin_memory()
+                st_[:, :, :cols] = x.cpu()
+                return st_[:, :, :cols], st_.numel() * 2
+            st_ = torch.empty(batch, cols, ld8(rows), dtype=torch.float16).pin_memory()
+            st_[:, :, :rows] = x.transpose(1, 2).cpu()
+            return st_[:, :, :rows].transpose(1, 2), st_.numel() * 2
+        hA = [host_copy(A, lay[0]) for lay, A, B in ops]
+        hB = [host_copy(B, lay[1]) for lay, A, B in ops]
+        Ah, Bh = [x for x, _ in hA], [x for x, _ in hB]
         bh = bias.cpu().pin_memory()
         sh = scale.cpu().pin_memory() if scale is not None else None
-        Ch = torch.empty(batch, M, N, dtype=torch.float16).pin_memory()
+        Ch = torch.empty(batch, M, ld8(N), dtype=torch.float16).pin_memory()[:, :, :N]
 
         def e2e_step():
             for i in range(len(ops)):
@@ -321,9 +359,9 @@ def run_ours(args):
             tt = torch.tensor([ems], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        h2d = sum(a.numel() * 2 + b.numel() * 2 + bh.numel() * 2 + (sh.numel() * 4 if sh is not None else 0)
-                  for a, b in zip(Ah, Bh))
-        d2h = len(ops) * Ch.numel() * 2
+        h2d = sum(na + nb + bh.numel() * 2 + (sh.numel() * 4 if sh is not None else 0)
+                  for (_, na), (_, nb) in zip(hA, hB))
+        d2h = len(ops) * batch * M * N * 2
         e2e = {"value": flop_per_launch * len(ops) * args.e2e_steps * world / (ems * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
                "path": "gemm_epilogue_host (C ABI, pinned host buffers)"}
@@ -347,11 +385,12 @@ def run_ours(args):
                     "frac_of_sustained": (achieved / peak_sus) if peak_sus else None,
                     "frac_of_spec_2250": achieved / 2250.0,
                     "kernel": "ge_fused_kernel (one launch per GEMM)",
-                    "kernel_avg_ms": kern_avg_ms, "kernel_share_of_step": sum(kern_ms) / (ms * (1 if world == 1 else 1)),
+                    "kernel_avg_ms": kern_avg_ms,
+                    "launch_mode": "CUDA graph replay per step" if graphs is not None else "eager",
                     "traffic_source": tsrc}
         comparators = None
         if not args.no_comparators and batch == 1:
-            comparators = compare_torch(torch, ops, bias, M, N, K, stream)
+            comparators = compare_torch(torch, sets, bias, M, N, K, stream, iters=args.steps * len(layouts))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f16", "accumulate": "f32",
@@ -368,31 +407,41 @@ def run_ours(args):
     return 0
 
 
-def compare_torch(torch, ops, bias, M, N, K, stream):
-    """Library reference points on the same box, same operands (not the product):
+def compare_torch(torch, sets, bias, M, N, K, stream, iters=10):
+    """Library reference points on the same box and the same rotating operand sets (not the product):
     torch unfused matmul + add + relu (cuBLAS + 2 elementwise kernels, the paper's baseline shape,
-    PAPER.md:1255-1260) and torch._addmm_activation (cuBLASLt bias+ReLU epilogue)."""
+    PAPER.md:1255-1260), torch._addmm_activation (cuBLASLt bias+ReLU epilogue) and plain
+    torch.matmul.  Each is replayed from CUDA graphs like our step; first layout of each set."""
     out = {}
-    lay, A, B = ops[0]
-    a, b = A[0], B[0]
     fl = 2.0 * M * N * K
 
-    def t(fn, it=10):
-        for _ in range(3):
-            fn()
+    def t(fn, it=iters):
+        graphs = []
+        for cur in sets:
+            lay, A, B = cur[0]
+            a, b = A[0], B[0]
+            fn(a, b)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                fn(a, b)
+            graphs.append(gr)
+        for i in range(3):
+            graphs[i % len(graphs)].replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(it):
-            fn()
+        for i in range(it):
+            graphs[i % len(graphs)].replay()
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / it * 1e-3
     try:
-        out["torch_unfused_matmul_add_relu"] = fl / t(lambda: torch.relu_(torch.matmul(a, b).add_(bias))) / 1e12
-        out["torch_matmul_only"] = fl / t(lambda: torch.matmul(a, b)) / 1e12
-        out["cublaslt_addmm_relu"] = fl / t(lambda: torch._addmm_activation(bias, a, b)) / 1e12
-        out["layout"] = lay
+        out["torch_unfused_matmul_add_relu"] = fl / t(lambda a, b: torch.relu_(torch.matmul(a, b).add_(bias))) / 1e12
+        out["torch_matmul_only"] = fl / t(lambda a, b: torch.matmul(a, b)) / 1e12
+        out["cublaslt_addmm_relu"] = fl / t(lambda a, b: torch._addmm_activation(bias, a, b)) / 1e12
+        out["layout"] = sets[0][0][0]
+        out["protocol"] = (f"CUDA graph replay, same rotating operand sets, {iters} launches each "
+                           "(as many as our timed region)")
     except Exception as e:  # pragma: no cover
         out["error"] = str(e)
     return out

@@ -201,7 +201,11 @@ Plan make_plan(const Args& a, int sms) {
         const int64_t conc = std::max(1, sms / cg);
         const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
         const double kk = static_cast<double>(std::max<int64_t>(a.K, 64)) + (bn == 512 ? kExposedK : 0.0);
-        const double cost = waves * (128.0 * bn) * kk / config_eff(bn, cg);
+        double eff = config_eff(bn, cg);
+        // The prologue transform rewrites each 16 KB A stage in smem: configurations with less MMA
+        // time per stage than 256 x 512 pair tiles become shared-memory bound.
+        if (a.o.prologue != GE_PRO_NONE && bn * cg < 1024) eff *= 0.55;
+        const double cost = waves * (128.0 * bn) * kk / eff;
         if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
             best = Plan{bn, cg, ge::stages_for(bn, cg), tiles};
             best_cost = cost;

@@ -533,21 +533,57 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     } else if (PRO && warp >= 4 + EPI_WARPS) {
         // ===================== prologue transform of the A stage (in place, in smem) ==========
         const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
+        // Thread xt rewrites the 16-B chunks o = (i*128 + xt)*16, i = 0..7, of each 16 KB A stage.
+        //  K-major stage (row = m, 128-B rows of 64 k, 128-B swizzle): the logical k-chunk of all
+        //   eight chunks is kc = (xt % 8) ^ ((xt / 8) % 8), so the thread needs scale[k0+8kc .. +8];
+        //  MN-major stage (row = k, 64-m atoms of 8 KB): chunk i lies on k = k0 + (16i + xt/8) % 64.
+        // The 8 scale values of the NEXT k-block are prefetched while the current one is
+        // transformed (the scale vector would otherwise cost an L2 round trip per chunk).
+        const bool scale_k = p.prologue == PRO_SCALE_K;
+        const int kc = (xt & 7) ^ ((xt >> 3) & 7);
+        auto fetch = [&](int kb, float* dst) {
+            const int k0 = kb * kBK;
+            if constexpr (A_MN) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = k0 + ((i * 16 + (xt >> 3)) & 63);
+                    dst[i] = k < p.K ? __ldg(p.scale + k) : 0.0f;
+                }
+            } else {
+                const int k = k0 + kc * 8;
+                if (p.scale_vec && k + 8 <= p.K) {
+                    const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + k));
+                    const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + k + 4));
+                    dst[0] = s0.x; dst[1] = s0.y; dst[2] = s0.z; dst[3] = s0.w;
+                    dst[4] = s1.x; dst[5] = s1.y; dst[6] = s1.z; dst[7] = s1.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) dst[e] = (k + e < p.K) ? __ldg(p.scale + k + e) : 0.0f;
+                }
+            }
+        };
+        float sc_cur[8], sc_nxt[8];
+        if (scale_k && nkb > 0) fetch(0, sc_nxt);
         int s = 0;
         uint32_t phase = 0;
         for (long long t = cluster_id; t < p.num_tiles; t += num_clusters) {
             for (int kb = 0; kb < nkb; ++kb) {
+                if (scale_k) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) sc_cur[e] = sc_nxt[e];
+                    fetch(kb + 1 < nkb ? kb + 1 : 0, sc_nxt);        // in flight during this stage
+                }
                 ptx::mbar_wait(&full_bar[s], phase);
                 uint8_t* sa = smem_a + s * C_::kAStage;
-                const int k0 = kb * kBK;
-#pragma unroll 2
-                for (int i = 0; i < C_::kAStage / 16 / 128; ++i) {
-                    const int o = (i * 128 + xt) * 16;               // byte offset of a 16-B chunk
-                    uint4 x = *reinterpret_cast<uint4*>(sa + o);
-                    __half2* h2 = reinterpret_cast<__half2*>(&x);
-                    if (p.prologue == PRO_RELU) {
-                        // a' = max(a, +0): clear every lane with the sign bit set (exact, -0 -> +0)
-                        uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+                constexpr int NCH = C_::kAStage / 16 / 128;          // 8 chunks per thread
+                uint4 x[NCH];
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) x[i] = *reinterpret_cast<const uint4*>(sa + (i * 128 + xt) * 16);
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) {
+                    if (!scale_k) {
+                        // RELU: a' = max(a, +0): clear every lane with the sign bit set (exact, -0 -> +0)
+                        uint32_t* w = reinterpret_cast<uint32_t*>(&x[i]);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             uint32_t u = w[e];
@@ -556,36 +592,19 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             w[e] = u;
                         }
                     } else {
-                        float sc[8];
-                        if constexpr (A_MN) {
-                            // MN-major stage: 128-B rows are K, the 8 values share one k.
-                            const int k = k0 + (o & 8191) / 128;
-                            const float sv = k < p.K ? __ldg(p.scale + k) : 0.0f;
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) sc[e] = sv;
-                        } else {
-                            // K-major stage: row m = o / 128, swizzled chunk -> logical k chunk.
-                            const int r = o / 128;
-                            const int kc = ((o / 16) & 7) ^ (r & 7);
-                            const int k = k0 + kc * 8;
-                            if (p.scale_vec && k + 8 <= p.K) {
-                                const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + k));
-                                const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + k + 4));
-                                sc[0] = s0.x; sc[1] = s0.y; sc[2] = s0.z; sc[3] = s0.w;
-                                sc[4] = s1.x; sc[5] = s1.y; sc[6] = s1.z; sc[7] = s1.w;
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) sc[e] = (k + e < p.K) ? __ldg(p.scale + k + e) : 0.0f;
-                            }
-                        }
+                        // SCALE_K: a' = RNE_fp16(s_k * a) (DESIGN.md R-C12)
+                        __half2* h2 = reinterpret_cast<__half2*>(&x[i]);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float2 a = __half22float2(h2[e]);
-                            h2[e] = __floats2half2_rn(sc[2 * e] * a.x, sc[2 * e + 1] * a.y);
+                            const float s0 = A_MN ? sc_cur[i] : sc_cur[2 * e];
+                            const float s1 = A_MN ? sc_cur[i] : sc_cur[2 * e + 1];
+                            h2[e] = __floats2half2_rn(s0 * a.x, s1 * a.y);
                         }
                     }
-                    *reinterpret_cast<uint4*>(sa + o) = x;
                 }
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) *reinterpret_cast<uint4*>(sa + (i * 128 + xt) * 16) = x[i];
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
