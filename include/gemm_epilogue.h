@@ -85,7 +85,15 @@ typedef struct {
     int32_t out_dtype;              /* ge_out_dtype */
     int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128, 256; 512 with cta_group 2) */
     int32_t cta_group;              /* 0 = heuristic; 1 = single-CTA tiles; 2 = CTA-pair tiles */
-} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0} */
+    int32_t stream_k;               /* 0 = heuristic; 1 = off; 2 = on whenever the last wave is partial */
+    void* workspace;                /* optional device workspace for stream-K partials (see ge_plan's
+                                       workspace_bytes); 16-byte aligned, ZERO-FILLED before its first
+                                       use and left zero-filled by every launch; must not be shared by
+                                       launches that may run concurrently.  NULL = library-managed
+                                       per-device buffer (then stream-K launches on different streams of
+                                       one device must not run concurrently; stream_k = 1 disables it). */
+    int64_t workspace_bytes;
+} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0} */
 
 typedef enum {
     GE_OK = 0,
@@ -161,13 +169,16 @@ const char* ge_status_string(ge_status status);
 const char* ge_last_error_detail(void);
 
 /*
- * Describes the configuration the heuristic picks for a shape (no device access):
- * writes tile_m, tile_n, cta_group, stages and the number of output tiles.
+ * Describes the configuration the heuristic picks for a shape (no device access): tile_m,
+ * tile_n, cta_group, pipeline stages, the number of output tiles, how many of them run
+ * stream-K (the last partial wave's tiles, whose K range is split evenly across all clusters;
+ * partial sums are reduced in fixed order, so results stay run-to-run deterministic) and the
+ * workspace bytes that needs.  Any output pointer may be NULL.
  */
 ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                   const ge_options* opt, int32_t num_sms,
                   int32_t* tile_m, int32_t* tile_n, int32_t* cta_group, int32_t* stages,
-                  int64_t* num_tiles);
+                  int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes);
 
 /* Number of fused kernels this library has launched in this process (for launch accounting). */
 uint64_t ge_launch_count(void);

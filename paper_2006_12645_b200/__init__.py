@@ -46,7 +46,8 @@ PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
 class GEOptions(ctypes.Structure):
     _fields_ = [("bias_mode", ctypes.c_int32), ("ldbias", ctypes.c_int64), ("prologue", ctypes.c_int32),
                 ("prologue_scale", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("tile_n", ctypes.c_int32),
-                ("cta_group", ctypes.c_int32)]
+                ("cta_group", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_int64)]
 
 
 class GEError(RuntimeError):
@@ -87,7 +88,8 @@ def load_library():
     lib.ge_last_error_detail.argtypes = []
     lib.ge_plan.restype = I32
     lib.ge_plan.argtypes = [I64, I64, I64, I64, I32, I32, OPT, I32, ctypes.POINTER(I32), ctypes.POINTER(I32),
-                            ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64)]
+                            ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64),
+                            ctypes.POINTER(I64)]
     lib.ge_launch_count.restype = ctypes.c_uint64
     lib.ge_launch_count.argtypes = []
     lib.ge_debug_read.restype = I32
@@ -117,8 +119,31 @@ def layout_of(x: torch.Tensor):
     raise ValueError(f"operand with shape {tuple(x.shape)} and strides {x.stride()} is neither row- nor column-major")
 
 
-def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group):
+_workspaces = {}
+
+
+def _workspace(device, stream_handle):
+    """Zero-filled stream-K workspace for (device, stream), large enough for any plan (one fp32
+    128 x 256 slot + one flag per SM).  Allocated through torch, so it is CUDA-graph safe; every
+    launch leaves it zero-filled."""
+    key = (device.index, int(stream_handle))
+    ws = _workspaces.get(key)
+    if ws is None:
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        ws = torch.zeros(sms * (128 * 256 * 4 + 4), dtype=torch.uint8, device=device)
+        _workspaces[key] = ws
+    return ws
+
+
+def clear_workspaces():
+    _workspaces.clear()
+
+
+def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, stream_k=0, ws=None):
     o = GEOptions()
+    o.stream_k = int(stream_k)
+    o.workspace = ws.data_ptr() if ws is not None else None
+    o.workspace_bytes = ws.numel() if ws is not None else 0
     o.bias_mode = BIAS_MODE[bias_mode]
     o.ldbias = int(ldbias or 0)
     o.prologue = PROLOGUE[prologue]
@@ -156,7 +181,7 @@ def _bias_ld(bias, bias_mode):
 def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None, *, op: Optional[str] = None,
                   bias_mode: str = "row", prologue: Optional[str] = None, scale: Optional[torch.Tensor] = None,
                   out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
-                  cta_group: int = 0, stream=None) -> torch.Tensor:
+                  cta_group: int = 0, stream_k: int = 0, stream=None) -> torch.Tensor:
     """C = relu_add(prologue(A) @ B, bias) on the current CUDA device (fp16 in, fp32 accumulate).
 
     A: (M, K) fp16, B: (K, N) fp16, row- or column-major views.  bias: (N,) for bias_mode "row",
@@ -178,10 +203,12 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     if out.stride(-1) != 1 and N > 1:
         raise ValueError("out must be row-major")
     ldbias, _ = _bias_ld(bias, bias_mode)
-    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group)
+    sh = _stream(stream)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
+                 _workspace(A.device, sh) if stream_k != 1 else None)
     st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
                            bias.data_ptr() if bias is not None else None, out.data_ptr(), max(out.stride(0), N, 1),
-                           _op(op, bias), ctypes.byref(o), _stream(stream))
+                           _op(op, bias), ctypes.byref(o), sh)
     _check(st)
     return out
 
@@ -203,18 +230,19 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
                           op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
                           scale: Optional[torch.Tensor] = None, out_dtype: torch.dtype = torch.float16,
                           out: Optional[torch.Tensor] = None, tile_n: int = 0, cta_group: int = 0,
-                          stream=None) -> torch.Tensor:
+                          stream_k: int = 0, stream=None) -> torch.Tensor:
     """Strided-batched form: A (b, M, K), B (b, K, N), bias (N,)/(b, N) [row], (M,)/(b, M) [col],
     (M, ld)/(b, M, ld) [full]; a 1-D/2-D bias is shared by every item.  One persistent launch."""
     lib = load_library()
     batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A, B, bias, bias_mode, out)
     if out is None:
         out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
-    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group)
+    sh = _stream(stream)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
+                 _workspace(A.device, sh) if stream_k != 1 else None)
     st = lib.gemm_epilogue_batched(batch, M, N, K, la, lb, A.data_ptr(), lda, sA, B.data_ptr(), ldb, sB,
                                    bias.data_ptr() if bias is not None else None, sbias, out.data_ptr(),
-                                   max(out.stride(1), N, 1), out.stride(0), _op(op, bias), ctypes.byref(o),
-                                   _stream(stream))
+                                   max(out.stride(1), N, 1), out.stride(0), _op(op, bias), ctypes.byref(o), sh)
     _check(st)
     return out
 
@@ -223,7 +251,7 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
                        op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
                        scale: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                        out_dtype: torch.dtype = torch.float16, tile_n: int = 0, cta_group: int = 0,
-                       stream=None) -> torch.Tensor:
+                       stream_k: int = 0, stream=None) -> torch.Tensor:
     """End-to-end path through the C ABI with HOST (CPU, ideally pinned) tensors: the library copies
     the inputs to the device, runs the fused kernel and copies C back, synchronously."""
     lib = load_library()
@@ -234,7 +262,7 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
         out = torch.empty((batch, M, N) if A.dim() == 3 else (M, N), dtype=out_dtype,
                           pin_memory=A.is_pinned())
     out3 = out if out.dim() == 3 else out.unsqueeze(0)
-    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k)
     st = lib.gemm_epilogue_host(batch, M, N, K, la, lb, A3.data_ptr(), lda, sA, B3.data_ptr(), ldb, sB,
                                 bias.data_ptr() if bias is not None else None, sbias, out3.data_ptr(),
                                 max(out3.stride(1), N, 1), out3.stride(0), _op(op, bias), ctypes.byref(o),
@@ -249,17 +277,17 @@ def validate_args(*args) -> int:
 
 
 def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: int = 148, tile_n: int = 0,
-         cta_group: int = 0) -> dict:
+         cta_group: int = 0, stream_k: int = 0, prologue: Optional[str] = None) -> dict:
     lib = load_library()
-    o = _options("row", 0, None, None, torch.float16, tile_n, cta_group)
+    o = _options("row", 0, prologue, None, torch.float16, tile_n, cta_group, stream_k)
     tm, tn, cg, stg = (ctypes.c_int32() for _ in range(4))
-    nt = ctypes.c_int64()
+    nt, sk, wsb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     st = lib.ge_plan(batch, M, N, K, 0 if layouts[0] == "r" else 1, 0 if layouts[1] == "r" else 1, ctypes.byref(o),
                      num_sms, ctypes.byref(tm), ctypes.byref(tn), ctypes.byref(cg), ctypes.byref(stg),
-                     ctypes.byref(nt))
+                     ctypes.byref(nt), ctypes.byref(sk), ctypes.byref(wsb))
     _check(st)
     return {"tile_m": tm.value, "tile_n": tn.value, "cta_group": cg.value, "stages": stg.value,
-            "num_tiles": nt.value}
+            "num_tiles": nt.value, "stream_k_tiles": sk.value, "workspace_bytes": wsb.value}
 
 
 def launch_count() -> int:
@@ -273,8 +301,9 @@ def debug_stats(max_ctas: int = 148):
     buf = np.zeros((max_ctas, 16), dtype=np.uint64)
     n = load_library().ge_debug_read(buf.ctypes.data, max_ctas)
     keys = ("total", "prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0",
-            "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math")
-    return [dict(zip(keys, (int(x) for x in buf[i, :10]))) for i in range(n)]
+            "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math", "sk_owner_wait", "sk_partial_write",
+            "sk_pieces", "epi_end")
+    return [dict(zip(keys, (int(x) for x in buf[i, :14]))) for i in range(n)]
 
 
 def version() -> str:

@@ -112,6 +112,9 @@ ge_status validate(Args& a) {
     if (o.cta_group < 0 || o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
     if (o.cta_group == 2 && o.tile_n == 64) return fail(GE_ERR_INVALID_VALUE, "cta_group 2 needs tile_n >= 128");
     if (o.cta_group == 1 && o.tile_n == 512) return fail(GE_ERR_INVALID_VALUE, "tile_n 512 needs cta_group 2");
+    if (o.stream_k < 0 || o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
+    if (o.workspace_bytes < 0 || (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 15)))
+        return fail(GE_ERR_INVALID_VALUE, "workspace must be 16-byte aligned with a non-negative size");
     // packed defaults
     const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
     const int64_t minlda = arow ? a.K : a.M, minldb = brow ? a.N : a.K;
@@ -171,6 +174,8 @@ ge_status validate(Args& a) {
 struct Plan {
     int bn, cg, stages;
     int64_t tiles;
+    int64_t sk_tiles;      // tiles of the last, partial wave split stream-K across all clusters (0 = none)
+    int64_t clusters;      // persistent clusters launched
 };
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -190,28 +195,91 @@ double config_eff(int bn, int cg) {
 // narrow tiles to fill the 148 SMs; large ones the CTA-pair tiles.
 Plan make_plan(const Args& a, int sms) {
     constexpr double kExposedK = 192.0;      // accumulator drain of a single-buffered tile, in K units
+    // Partial write + flag handshake + read-back of a stream-K share, in K units: measured ~25K
+    // cycles on B200 (profiles/r01_stream_k.txt), i.e. about 50 k-blocks of a 256 x 256 pair tile.
+    constexpr double kStreamKCostK = 3200.0;
     Plan best{};
     double best_cost = 0;
     const int cands[6][2] = {{512, 2}, {256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
+    const int64_t nkb = cdiv(a.K, 64);
     for (const auto& c : cands) {
         const int bn = c[0], cg = c[1];
         if (a.o.tile_n && a.o.tile_n != bn) continue;
         if (a.o.cta_group && a.o.cta_group != cg) continue;
+        // Skinny M (<= 64 rows): most of every A stage is TMA zero-fill, the shape is HBM bound on B
+        // and 128 x 128 tiles measure best (profiles/r01_tune_sweep.json); narrower tiles only add
+        // A-stage traffic per useful byte.
+        if (a.M <= 64 && !a.o.tile_n && !a.o.cta_group && !(bn == 128 && cg == 1)) continue;
         const int64_t tiles = a.batch * cdiv(a.M, 128 * cg) * cdiv(a.N, bn);
         const int64_t conc = std::max(1, sms / cg);
-        const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
         const double kk = static_cast<double>(std::max<int64_t>(a.K, 64)) + (bn == 512 ? kExposedK : 0.0);
         double eff = config_eff(bn, cg);
         // The prologue transform rewrites each 16 KB A stage in smem: configurations with less MMA
         // time per stage than 256 x 512 pair tiles become shared-memory bound.
         if (a.o.prologue != GE_PRO_NONE && bn * cg < 1024) eff *= 0.55;
-        const double cost = waves * (128.0 * bn) * kk / eff;
+        // data-parallel: whole waves of tiles
+        const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
+        double cost = waves * (128.0 * bn) * kk / eff;
+        int64_t sk = 0;
+        // stream-K for the last partial wave (double-buffered accumulators only)
+        const int64_t rem = tiles % conc;
+        const bool sk_ok = bn <= 256 && rem != 0 && nkb >= 2 && a.o.stream_k != 1;
+        if (sk_ok) {
+            const double sk_waves = static_cast<double>(tiles / conc) + static_cast<double>(rem) / conc;
+            const double sk_cost = (sk_waves * kk + kStreamKCostK) * (128.0 * bn) / eff;
+            if (a.o.stream_k == 2 || sk_cost < cost) {
+                cost = sk_cost;
+                sk = rem;
+            }
+        }
         if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
-            best = Plan{bn, cg, ge::stages_for(bn, cg), tiles};
+            best = Plan{bn, cg, ge::stages_for(bn, cg), tiles, sk, sk ? conc : std::min<int64_t>(tiles, conc)};
             best_cost = cost;
         }
     }
+    best.clusters = std::max<int64_t>(best.clusters, 1);
     return best;
+}
+
+// Stream-K workspace: one fp32 128 x BN slot per CTA plus one flag per CTA (flags must start at 0;
+// every launch leaves them at 0).
+size_t sk_workspace_bytes(const Plan& pl) {
+    if (!pl.sk_tiles) return 0;
+    const size_t ctas = static_cast<size_t>(pl.clusters * pl.cg);
+    return ctas * 128 * pl.bn * 4 + ctas * 4;
+}
+
+struct SkWorkspace {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_sk_mu;
+SkWorkspace g_sk[64];
+
+// Library-managed stream-K workspace of the current device (used when the caller passes none).
+void* sk_library_workspace(size_t need, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_sk_mu);
+    SkWorkspace& w = g_sk[dev & 63];
+    if (w.bytes >= need) return w.ptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (cap != cudaStreamCaptureStatusNone) return nullptr;       // cannot allocate while capturing
+    if (w.ptr) {
+        cudaDeviceSynchronize();
+        cudaFree(w.ptr);
+        w.ptr = nullptr;
+        w.bytes = 0;
+    }
+    if (cudaMalloc(&w.ptr, need) != cudaSuccess || cudaMemset(w.ptr, 0, need) != cudaSuccess) {
+        cudaGetLastError();
+        w.ptr = nullptr;
+        return nullptr;
+    }
+    cudaDeviceSynchronize();
+    w.bytes = need;
+    return w.ptr;
 }
 
 // Raster group: tiles are walked in groups of `group_m` tile-rows so the tiles in flight share
@@ -360,8 +428,31 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.dbg_flags = dflags;
     if (dflags & 4) p.c_tma = 0;                  // experiment: st.global epilogue instead of TMA stores
 
-    const int64_t clusters = std::min<int64_t>(pl.tiles, sms / pl.cg);
-    const int grid = static_cast<int>(std::max<int64_t>(clusters, 1) * pl.cg);
+    // stream-K (last partial wave split across all clusters) when a workspace is available
+    Plan plan = pl;
+    p.dp_tiles = plan.tiles;
+    p.sk_units = 0;
+    p.sk_ws = nullptr;
+    p.sk_flags = nullptr;
+    if (plan.sk_tiles) {
+        const size_t need = sk_workspace_bytes(plan);
+        void* ws = nullptr;
+        if (a.o.workspace) {
+            if (static_cast<size_t>(a.o.workspace_bytes) >= need) ws = a.o.workspace;
+        } else {
+            ws = sk_library_workspace(need, st);
+        }
+        if (ws) {
+            const size_t ctas = static_cast<size_t>(plan.clusters * plan.cg);
+            p.sk_ws = static_cast<float*>(ws);
+            p.sk_flags = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + ctas * 128 * plan.bn * 4);
+            p.dp_tiles = plan.tiles - plan.sk_tiles;
+            p.sk_units = plan.sk_tiles * p.num_k_blocks;
+        } else {
+            plan.clusters = std::min<int64_t>(plan.tiles, sms / plan.cg);     // data-parallel fallback
+        }
+    }
+    const int grid = static_cast<int>(std::max<int64_t>(plan.clusters, 1) * plan.cg);
     cudaError_t e;
     if (pl.cg == 1) {
         if (pl.bn == 64) e = ge::launch_cg1_bn64(a_mn, b_mn, f32, pro, maps, p, grid, st);
@@ -385,7 +476,7 @@ Args make_args(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t la, int32
                int64_t ldc, int64_t sC, int32_t op, const ge_options* opt) {
     Args a{batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op, {}};
     if (opt) a.o = *opt;
-    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0};
+    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0};
     return a;
 }
 
@@ -552,7 +643,7 @@ const char* ge_last_error_detail(void) { return g_detail.c_str(); }
 
 ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                   const ge_options* opt, int32_t num_sms, int32_t* tile_m, int32_t* tile_n, int32_t* cta_group,
-                  int32_t* stages, int64_t* num_tiles) {
+                  int32_t* stages, int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes) {
     g_detail.clear();
     Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0,
                        GE_EPI_NONE, opt);
@@ -560,12 +651,15 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 256 && a.o.tile_n != 512)
         return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 256 or 512");
     if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
+    if (a.o.stream_k < 0 || a.o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
     const Plan p = make_plan(a, num_sms);
     if (tile_m) *tile_m = 128 * p.cg;
     if (tile_n) *tile_n = p.bn;
     if (cta_group) *cta_group = p.cg;
     if (stages) *stages = p.stages;
     if (num_tiles) *num_tiles = p.tiles;
+    if (stream_k_tiles) *stream_k_tiles = p.sk_tiles;
+    if (workspace_bytes) *workspace_bytes = static_cast<int64_t>(sk_workspace_bytes(p));
     return GE_OK;
 }
 

@@ -64,6 +64,12 @@ struct Params {
     int c_vec;                      // st.global path may use 16-B vector stores (aligned rows)
     // L2 eviction priority of the operand loads / output stores (0 normal, 1 first, 2 last)
     int hint_a, hint_b, hint_c;
+    // stream-K: tiles [dp_tiles, num_tiles) are split into sk_units
+    // k-block units shared evenly by all clusters; partial accumulators go to sk_ws (one fp32
+    // 128 x BN slot per CTA), announced through sk_flags (one per CTA, reset by the consumer)
+    long long dp_tiles, sk_units;
+    float* sk_ws;
+    unsigned int* sk_flags;
     // diagnostics (GE_DEBUG_STATS): per-CTA blocked-cycle counters, or nullptr
     unsigned long long* dbg;
     int dbg_noload;                 // dev experiment only: stop issuing TMA after the ring is full once
@@ -73,7 +79,8 @@ struct Params {
 // Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
 enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
              DBG_EPI_REL0 = 5, DBG_EPI_REL1 = 6, DBG_EPI_TILE = 7, DBG_EPI_TMEMLD = 8,
-             DBG_EPI_MATH = 9, DBG_SLOTS = 16 };
+             DBG_EPI_MATH = 9, DBG_SK_WAIT = 10, DBG_SK_WRITE = 11, DBG_SK_PIECES = 12, DBG_EPI_END = 13,
+             DBG_MMA_END = 14, DBG_SLOTS = 16 };
 
 template <int BN, int CG>
 struct Cfg {
@@ -117,6 +124,70 @@ __device__ __forceinline__ void decode_tile(const Params& p, long long t, int ti
     nt = rr / gsz;
     (void)tile_m;
 }
+
+// Work of one cluster, in the order the producer and MMA process it: data-parallel tiles
+// t = cid, cid + G, ... < dp_tiles, then the cluster's share [u0, u1) of the stream-K units
+// (k-blocks of tiles dp_tiles .. num_tiles-1, tile-major), cut at tile boundaries.  The host keeps
+// the stream-K tiles fewer than the clusters, so a share spans at most two pieces.
+enum : int { PIECE_FULL = 0, PIECE_OWNER = 1, PIECE_PARTIAL = 2 };
+struct Piece {
+    long long tile;
+    int kb0, kb1;                   // k-block range [kb0, kb1) of the tile
+    int kind;                       // FULL (whole tile), OWNER (holds the tile's last k-block), PARTIAL
+};
+
+struct WorkSeq {
+    long long dp_tiles, units, u0, u1;
+    int cid, G, nkb, n_dp, n_sk;
+    __device__ __forceinline__ WorkSeq(const Params& p, int cid_, int G_) {
+        cid = cid_;
+        G = G_;
+        nkb = p.num_k_blocks;
+        dp_tiles = p.dp_tiles;
+        units = p.sk_units;
+        n_dp = dp_tiles > cid ? static_cast<int>((dp_tiles - cid + G - 1) / G) : 0;
+        u0 = range_begin(cid);
+        u1 = range_begin(cid + 1);
+        n_sk = 0;
+        if (u1 > u0) n_sk = (u1 > (u0 / nkb + 1) * nkb) ? 2 : 1;
+    }
+    __device__ __forceinline__ long long range_begin(int c) const { return units * c / G; }
+    __device__ __forceinline__ int count() const { return n_dp + n_sk; }
+    __device__ __forceinline__ Piece get(int i) const {
+        Piece pc;
+        if (i < n_dp) {
+            pc.tile = cid + static_cast<long long>(i) * G;
+            pc.kb0 = 0;
+            pc.kb1 = nkb;
+            pc.kind = PIECE_FULL;
+            return pc;
+        }
+        // With two pieces, the PARTIAL head of the next tile is processed first and the tail of the
+        // current tile (OWNER or FULL) last, so every partial is published while its cluster's
+        // MMAs are still busy and owners never wait at the end of the kernel.
+        const long long split = (u0 / nkb + 1) * nkb;
+        const long long u = (n_sk == 2) ? ((i == n_dp) ? split : u0) : u0;
+        const long long rel = u / nkb;
+        const long long end = u1 < (rel + 1) * nkb ? u1 : (rel + 1) * nkb;
+        pc.tile = dp_tiles + rel;
+        pc.kb0 = static_cast<int>(u - rel * nkb);
+        pc.kb1 = static_cast<int>(end - rel * nkb);
+        pc.kind = (pc.kb0 == 0 && pc.kb1 == nkb) ? PIECE_FULL : (pc.kb1 == nkb ? PIECE_OWNER : PIECE_PARTIAL);
+        return pc;
+    }
+    // Partial pieces come first in every cluster's order, so a partial is never behind an owner
+    // wait (no wait chains across clusters); the epilogue follows the MMA order.
+    __device__ __forceinline__ int epi_index(int j) const { return j; }
+    // Clusters holding the other pieces of stream-K tile `tile` are the NON-EMPTY ranges among
+    // [first_contributor, cid): every cluster whose range ends after the tile's first unit.
+    __device__ __forceinline__ int first_contributor(long long tile) const {
+        const long long x0 = (tile - dp_tiles) * nkb;
+        int c = cid;
+        while (c > 0 && range_begin(c) > x0) --c;      // range_begin(c) <= x0 < range_end(c) unless empty
+        return c;
+    }
+    __device__ __forceinline__ bool has_units(int c) const { return range_begin(c + 1) > range_begin(c); }
+};
 
 // fp32 epilogue value: v = acc + beta, then relu (y = v > 0 ? v : +0, DESIGN.md R-C5).
 __device__ __forceinline__ float epi(float acc, float beta, int relu) {
@@ -194,6 +265,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     const int cluster_id = blockIdx.x / CG;
     const int num_clusters = gridDim.x / CG;
     const int nkb = p.num_k_blocks;
+    const WorkSeq work(p, cluster_id, num_clusters);
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -202,17 +274,19 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             uint32_t phase = 0;
             const uint64_t pol_a = ptx::l2_policy(p.hint_a);
             const uint64_t pol_b = ptx::l2_policy(p.hint_b);
-            for (long long t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            for (int wi = 0; wi < work.count(); ++wi) {
+                const Piece pc = work.get(wi);
+                const long long t = pc.tile;
                 int b, mt, nt;
                 decode_tile(p, t, C_::kTileM, b, mt, nt);
                 const int m0 = mt * C_::kTileM + rank * kRowsPerCta;
                 const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
-                for (int kb = 0; kb < nkb; ++kb) {
+                for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                     ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg ? &dbg[DBG_PROD_EMPTY] : nullptr);
                     const int k0 = kb * kBK;
                     uint8_t* sa = smem_a + s * C_::kAStage;
                     uint8_t* sb = smem_b + s * C_::kBStage;
-                    if (p.dbg_noload && (t != cluster_id || kb >= S)) {
+                    if (p.dbg_noload && (wi != 0 || kb >= S)) {
                         // timing experiment (GE_DEBUG_NOLOAD): operands stay resident, results invalid
                         if (CG == 1 || PRO || leader) ptx::mbar_arrive(&full_bar[s]);
                         if (++s == S) { s = 0; phase ^= 1; }
@@ -264,11 +338,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             const uint32_t b_base = ptx::smem_u32(smem_b);
             int s = 0, it = 0;
             uint32_t phase = 0;
-            for (long long t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+            for (; it < work.count(); ++it) {
+                const Piece pc = work.get(it);
                 const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
                 const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < nkb; ++kb) {
+                for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                     ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
                     ptx::tc_fence_after();
                     const uint32_t sa = a_base + s * C_::kAStage;
@@ -282,9 +357,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                                                  : ptx::make_sw128_desc(sa + k * 32, 0, 1024);
                         const uint64_t bd = B_MN ? ptx::make_sw128_desc(sbh + k * 2048, 8192, 1024)
                                                  : ptx::make_sw128_desc(sbh + k * 32, 0, 1024);
-                        ptx::mma_f16_elect<CG>(d_tmem + h * C_::kUmmaN, ad, bd, IDESC, (kb | k) != 0);
+                        ptx::mma_f16_elect<CG>(d_tmem + h * C_::kUmmaN, ad, bd, IDESC, (kb != pc.kb0) || k != 0);
                     };
-                    if (kb == 0) {
+                    if (kb == pc.kb0) {
                         // first k-block of a tile: start on accumulator half 0 as soon as the
                         // epilogue has drained it, then wait for half 1
 #pragma unroll
@@ -307,7 +382,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             for (int h = 0; h < NH; ++h) mma_one(h, k);
                     }
                     ptx::mma_commit_elect<CG>(&empty_bar[s]);    // smem slot free once these MMAs finish
-                    if (kb == nkb - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
+                    if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
                     if (++s == S) { s = 0; phase ^= 1; }
                 }
             }
@@ -335,8 +410,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         uint8_t* stage_c = smem_c + e_idx * (NBUF * STG);
         const uint64_t pol_c = ptx::l2_policy(p.hint_c);
         int buf = 0;
-        int it = 0;
-        for (long long t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+        for (int jj = 0; jj < work.count(); ++jj) {
+            const int it = work.epi_index(jj);
+            const Piece pc = work.get(it);
+            const long long t = pc.tile;
             int b, mt, nt;
             decode_tile(p, t, C_::kTileM, b, mt, nt);
             const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
@@ -348,7 +425,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // the ~2 KB of L1 the smem carve-out leaves): the ROW slice goes to smem as fp32.
             float beta_col = 0.0f;
             if (p.bias_mode == BIAS_COL && row < p.M) beta_col = __half2float(bias_b[row]);
-            if (p.bias_mode == BIAS_ROW) {
+            if (p.bias_mode == BIAS_ROW && pc.kind != PIECE_PARTIAL) {
                 ptx::named_bar_sync(1, EPI_WARPS * 32);            // previous tile's reads are done
                 for (int i = threadIdx.x - 128; i < BN; i += EPI_WARPS * 32) {
                     const int col = nt * BN + i;
@@ -488,6 +565,73 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
             };
 
+            // ---- stream-K pieces (double-buffered configurations only)
+            // Workspace slot of a CTA: 128 x BN fp32 in [chunk][vec][row] float4 order (private
+            // layout), so the 32 lanes of a warp (32 consecutive rows) touch 512 contiguous bytes.
+            const int trow = q * 32 + lane;
+            auto ws_slot = [&](int cluster) {
+                return reinterpret_cast<float4*>(p.sk_ws) + static_cast<size_t>(cluster * CG + rank) * (kRowsPerCta * BN / 4);
+            };
+            int c_first = cluster_id;
+            if constexpr (C_::kAccStages == 2) {
+                if (dbg && e_idx == 0 && lane == 0 && pc.kind != PIECE_FULL) dbg[DBG_SK_PIECES] += 1;
+                if (pc.kind == PIECE_PARTIAL) {
+                    const long long tw0 = clock64();
+                    // partial accumulator -> this CTA's workspace slot (fp32, row = TMEM lane), then
+                    // publish it; bias and ReLU are applied once, by the owner, after the full
+                    // reduction (DESIGN.md R-C13)
+#pragma unroll 1
+                    for (int j = 0; j < CPH; ++j) {
+                        const int c = j * NG + grp;
+                        uint32_t v[W];
+                        load(c, v);
+                        ptx::tmem_ld_wait();
+                        if (j == CPH - 1) release(0);
+                        float4* dst = ws_slot(cluster_id) + static_cast<size_t>(c * (W / 4)) * kRowsPerCta + trow;
+#pragma unroll
+                        for (int g = 0; g < W / 4; ++g)
+                            __stcg(dst + g * kRowsPerCta,
+                                   make_float4(__uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]),
+                                               __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3])));
+                    }
+                    __threadfence();
+                    ptx::named_bar_sync(2, EPI_WARPS * 32);
+                    if (e_idx == 0 && lane == 0) ptx::st_release_gpu(p.sk_flags + cluster_id * CG + rank, 1u);
+                    if (dbg && e_idx == 0 && lane == 0) dbg[DBG_SK_WRITE] += static_cast<unsigned long long>(clock64() - tw0);
+                    continue;
+                }
+                if (pc.kind == PIECE_OWNER) {
+                    // wait until every earlier piece of this tile is in its cluster's workspace slot
+                    c_first = work.first_contributor(t);
+                    const long long tw0 = clock64();
+                    if (e_idx == 0 && lane == 0)
+                        for (int c2 = c_first; c2 < cluster_id; ++c2)
+                            if (work.has_units(c2)) ptx::spin_acquire_gpu(p.sk_flags + c2 * CG + rank, 1u);
+                    ptx::named_bar_sync(2, EPI_WARPS * 32);
+                    if (dbg && e_idx == 0 && lane == 0) dbg[DBG_SK_WAIT] += static_cast<unsigned long long>(clock64() - tw0);
+                }
+            }
+            // owner: add the published partials (ascending cluster order: deterministic)
+            auto add_partials = [&](const int c, uint32_t* v) {
+                if constexpr (C_::kAccStages == 2) {
+                    for (int c2 = c_first; c2 < cluster_id; ++c2) {
+                        if (!work.has_units(c2)) continue;
+                        const float4* src = ws_slot(c2) + static_cast<size_t>(c * (W / 4)) * kRowsPerCta + trow;
+                        float4 pvs[W / 4];
+#pragma unroll
+                        for (int g = 0; g < W / 4; ++g) pvs[g] = __ldcg(src + g * kRowsPerCta);
+#pragma unroll
+                        for (int g = 0; g < W / 4; ++g) {
+                            const float4 pv = pvs[g];
+                            v[4 * g] = __float_as_uint(__uint_as_float(v[4 * g]) + pv.x);
+                            v[4 * g + 1] = __float_as_uint(__uint_as_float(v[4 * g + 1]) + pv.y);
+                            v[4 * g + 2] = __float_as_uint(__uint_as_float(v[4 * g + 2]) + pv.z);
+                            v[4 * g + 3] = __float_as_uint(__uint_as_float(v[4 * g + 3]) + pv.w);
+                        }
+                    }
+                }
+            };
+
             if (p.dbg_flags & 1) {          // timing experiment: release without draining
 #pragma unroll
                 for (int h = 0; h < NH; ++h) release(h);
@@ -521,15 +665,26 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         load(c, v);
                         if (nkb > 0) ptx::tmem_ld_wait();
                         if (j == CPH - 1) release(h);
+                        if (pc.kind == PIECE_OWNER) add_partials(c, v);
                         uint32_t w[NWORD];
                         compute(c, v, w);
                         store(c, w);
                     }
                 }
             }
+            if constexpr (C_::kAccStages == 2) {
+                if (pc.kind == PIECE_OWNER) {
+                    // partials consumed: reset the contributors' flags for the next launch
+                    ptx::named_bar_sync(2, EPI_WARPS * 32);
+                    if (e_idx == 0 && lane == 0)
+                        for (int c2 = c_first; c2 < cluster_id; ++c2)
+                            if (work.has_units(c2)) ptx::st_relaxed_gpu(p.sk_flags + c2 * CG + rank, 0u);
+                }
+            }
             if (dbg && e_idx == 0 && lane == 0) dbg[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
         }
         if (p.c_tma && lane == 0) ptx::bulk_wait<0>();
+        if (dbg && e_idx == 0 && lane == 0) dbg[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
     } else if (PRO && warp >= 4 + EPI_WARPS) {
         // ===================== prologue transform of the A stage (in place, in smem) ==========
         const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
@@ -563,15 +718,18 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             }
         };
         float sc_cur[8], sc_nxt[8];
-        if (scale_k && nkb > 0) fetch(0, sc_nxt);
+        if (scale_k && nkb > 0 && work.count() > 0) fetch(work.get(0).kb0, sc_nxt);
         int s = 0;
         uint32_t phase = 0;
-        for (long long t = cluster_id; t < p.num_tiles; t += num_clusters) {
-            for (int kb = 0; kb < nkb; ++kb) {
+        for (int wi = 0; wi < work.count(); ++wi) {
+            const Piece pc = work.get(wi);
+            for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                 if (scale_k) {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) sc_cur[e] = sc_nxt[e];
-                    fetch(kb + 1 < nkb ? kb + 1 : 0, sc_nxt);        // in flight during this stage
+                    int kn = kb + 1;                                  // next k-block this thread transforms
+                    if (kn == pc.kb1) kn = (wi + 1 < work.count()) ? work.get(wi + 1).kb0 : 0;
+                    fetch(kn, sc_nxt);                                // in flight during this stage
                 }
                 ptx::mbar_wait(&full_bar[s], phase);
                 uint8_t* sa = smem_a + s * C_::kAStage;

@@ -5,17 +5,26 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2006_12645_b200 as ge
 M, N, K = (int(x) for x in sys.argv[1:4]); lay = sys.argv[4]; bn, cg = int(sys.argv[5]), int(sys.argv[6])
+sk = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 A = torch.randn(M, K, device="cuda", dtype=torch.float16); B = torch.randn(K, N, device="cuda", dtype=torch.float16)
 if lay[0] == "c": A = A.t().contiguous().t()
 if lay[1] == "c": B = B.t().contiguous().t()
 bias = torch.randn(N, device="cuda", dtype=torch.float16); C = torch.empty(M, N, device="cuda", dtype=torch.float16)
-for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg)
+for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk)
 torch.cuda.synchronize()
 st = ge.debug_stats()
 lead = [s for i, s in enumerate(st) if cg == 1 or i % 2 == 0]
 def avg(k, rows): return sum(r[k] for r in rows) / max(1, len(rows))
 tot = avg("total", lead)
 print(f"{M}x{N}x{K} {lay} bn={bn} cg={cg}: total {tot:.0f} cyc/CTA(leader)")
-for k in ("prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0", "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math"):
+for k in ("prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0", "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math", "sk_owner_wait", "sk_partial_write", "sk_pieces", "epi_end"):
     print(f"  {k:18s} {avg(k, lead):12.0f} cyc  ({100*avg(k, lead)/tot:5.1f}% of total)")
 print("  per-CTA mma_wait_full min/max:", min(r["mma_wait_full"] for r in lead), max(r["mma_wait_full"] for r in lead))
+
+ends = sorted(r["epi_end"] for r in st)
+print("  epi_end per CTA: min", ends[0], "median", ends[len(ends)//2], "max", ends[-1])
+tots = sorted(r["total"] for r in lead)
+print("  mma end (total) per leader: min", tots[0], "median", tots[len(tots)//2], "max", tots[-1])
+print("  slowest CTAs (idx: epi_end, mma_end(total), owner_wait, partial_write, pieces, epi_tile):")
+for i, r in sorted(enumerate(st), key=lambda x: -x[1]["epi_end"])[:6]:
+    print(f"    {i:3d}: {r['epi_end']:7d} {r['total']:7d} {r['sk_owner_wait']:7d} {r['sk_partial_write']:6d} {r['sk_pieces']} {r['epi_tile']:7d}")

@@ -1,0 +1,40 @@
+"""Dev: measured TF/s of every kernel configuration per shape (CUDA-graph timed, rotating operands),
+plus what the heuristic picks.  Output feeds config_eff / the plan cost model."""
+import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2006_12645_b200 as ge
+shapes = [(1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192), (5124, 704, 2048),
+          (35, 8464, 2560), (2048, 2048, 8192), (512, 512, 512)]
+cfgs = [(512, 2), (256, 2), (256, 1), (128, 2), (128, 1), (64, 1)]
+res = {}
+for (M, N, K) in shapes:
+    nsets = max(1, min(16, int(3 * 126e6 // (2 * (M * K + K * N))) + 1))
+    sets = [(torch.randn(M, K, device="cuda", dtype=torch.float16), torch.randn(K, N, device="cuda", dtype=torch.float16))
+            for _ in range(nsets)]
+    bias = torch.randn(N, device="cuda", dtype=torch.float16)
+    C = torch.empty(M, N, device="cuda", dtype=torch.float16)
+    row = {}
+    for bn, cg in cfgs + [(0, 0)]:
+        graphs = []
+        for A, B in sets:
+            ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(4):
+                    ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg)
+            graphs.append(g)
+        for g in graphs[:3]: g.replay()
+        torch.cuda.synchronize()
+        it = max(8, min(200, int(2e-1 / (2 * M * N * K / 1.2e15) / 4)))
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(it): graphs[i % nsets].replay()
+        e.record(); torch.cuda.synchronize()
+        t = s.elapsed_time(e) / (it * 4) * 1e-3
+        row["auto" if bn == 0 else f"{bn}x{cg}"] = round(2 * M * N * K / t / 1e12, 1)
+    pl = ge.plan(M, N, K)
+    row["auto_pick"] = f"{pl['tile_n']}x{pl['cta_group']}"
+    res[f"{M}x{N}x{K}"] = row
+    print(f"{M}x{N}x{K}", row, flush=True)
+json.dump(res, open("gpurun_out/tune_sweep.json", "w"), indent=1)

@@ -78,6 +78,7 @@ def v(lib, batch=1, M=128, N=128, K=64, la=0, lb=0, A=P, lda=0, sA=0, B=P * 16, 
 def opts(ge, **kw):
     o = ge.GEOptions()
     o.bias_mode, o.ldbias, o.prologue, o.prologue_scale, o.out_dtype, o.tile_n, o.cta_group = 0, 0, 0, None, 0, 0, 0
+    o.stream_k, o.workspace, o.workspace_bytes = 0, None, 0
     for k, val in kw.items():
         setattr(o, k, val)
     return o
@@ -117,7 +118,10 @@ def test_validate_invalid_values(lib, ge):
     assert v(lib, opt=opts(ge, cta_group=2, tile_n=64)) == S.INVALID_VALUE
     assert v(lib, opt=opts(ge, bias_mode=2, ldbias=64)) == S.INVALID_VALUE   # ldbias < N
     assert v(lib, batch=2, sC=100) == S.INVALID_VALUE   # output items would overlap
+    assert v(lib, opt=opts(ge, stream_k=3)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, workspace=P + 4, workspace_bytes=1 << 20)) == S.INVALID_VALUE   # misaligned
     assert lib.ge_last_error_detail()                    # a reason is recorded
+    assert v(lib, opt=opts(ge, workspace=P * 1024, workspace_bytes=1 << 20)) == 0
 
 
 def test_validate_alignment(lib, ge):
@@ -143,13 +147,21 @@ def test_plan_tiles(ge):
     assert p["tile_m"] == 128 and p["tile_n"] == 256 and p["num_tiles"] == 64 * 32
     p = ge.plan(8192, 8192, 8192, tile_n=256, cta_group=2)
     assert p["tile_m"] == 256 and p["num_tiles"] == 32 * 32
-    p = ge.plan(35, 8457, 2560)                        # skinny: heuristic narrows the N tile to fill the SMs
-    assert p["tile_n"] == 64 and p["num_tiles"] == 133
+    p = ge.plan(35, 8457, 2560)                        # skinny M: 128 x 128 tiles (measured best, HBM bound)
+    assert (p["tile_n"], p["cta_group"]) == (128, 1) and p["num_tiles"] == 67 and p["stream_k_tiles"] == 0
+    p = ge.plan(1024, 1024, 1024)                      # small: narrow tiles to fill the SMs
+    assert p["tile_n"] == 64 and p["num_tiles"] == 128
     p = ge.plan(2048, 2048, 2048, batch=64)           # large: the 256 x 256 CTA-pair tile
     assert p["cta_group"] == 2 and p["tile_n"] == 256 and p["num_tiles"] == 64 * 8 * 8
     assert p["stages"] >= 4
     p = ge.plan(8192, 8192, 8192)
     assert p["cta_group"] == 2 and p["tile_n"] in (256, 512)
+    # stream-K: only the last partial wave is split; workspace = one fp32 128 x BN slot + flag per CTA
+    p = ge.plan(4096, 4096, 4096, tile_n=256, cta_group=2, stream_k=2)
+    assert p["num_tiles"] == 256 and p["stream_k_tiles"] == 256 % 74
+    assert p["workspace_bytes"] == 148 * (128 * 256 * 4 + 4)
+    assert ge.plan(4096, 4096, 4096, tile_n=256, cta_group=2, stream_k=1)["stream_k_tiles"] == 0
+    assert ge.plan(8192, 8192, 8192, tile_n=512, cta_group=2, stream_k=2)["stream_k_tiles"] == 0   # 1-buffer acc
     with pytest.raises(ge.GEError):
         ge.plan(8192, 8192, 8192, tile_n=96)
 

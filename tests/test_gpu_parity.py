@@ -202,3 +202,58 @@ def test_host_entry_point():
     Cd = ge.gemm_epilogue(Ah.cuda(), Bh.t().contiguous().cuda().t(), prob.bias.cuda())
     torch.cuda.synchronize()
     assert torch.equal(Ch, Cd.cpu())
+
+
+# ------------------------------------------------------------------ stream-K
+@pytest.mark.parametrize("M,N,K,tile_n,cg", [(1024, 1024, 1024, 256, 2), (640, 3000, 960, 256, 2),
+                                            (2048, 768, 4096, 256, 1), (300, 520, 200, 128, 1),
+                                            (4096, 4096, 256, 256, 2), (512, 512, 128, 64, 1)])
+@pytest.mark.parametrize("layouts", ["rr", "cc"])
+def test_stream_k_exact_and_bound(M, N, K, tile_n, cg, layouts):
+    """Stream-K split of the last wave: bias+ReLU applied once after the full reduction (R-C13);
+    small integers stay bitwise exact, uniform data within the bound."""
+    p = ge.plan(M, N, K, tile_n=tile_n, cta_group=cg, stream_k=2)
+    assert p["stream_k_tiles"] > 0
+    for kind in ("smallint", "uniform"):
+        prob = workloads.make_problem(M, N, K, seed=41, kind=kind, bias_mode="row")
+        got = run_gpu(prob, layouts, tile_n=tile_n, cta_group=cg, stream_k=2)
+        out, mag = oracle_run(prob, layouts)
+        if kind == "smallint":
+            assert np.array_equal(got, exact_expect(out, torch.float16))
+        else:
+            check_bound(got, out, mag, f"stream-K {M}x{N}x{K}")
+
+
+def test_stream_k_deterministic_repeated_and_graph():
+    """Fixed-order partial reduction: bitwise reproducible across launches, across a CUDA graph
+    replay, and equal to the data-parallel result within the bound; flags are left reset."""
+    prob = workloads.make_problem(2048, 2048, 2048, seed=42, bias_mode="col")
+    A, B = dev_operands(prob, "rc")
+    bias = prob.bias.cuda()
+    kw = dict(bias_mode="col", tile_n=256, cta_group=2, stream_k=2)
+    c1 = ge.gemm_epilogue(A, B, bias, **kw)
+    c2 = ge.gemm_epilogue(A, B, bias, **kw)
+    out = torch.empty_like(c1)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ge.gemm_epilogue(A, B, bias, out=out, **kw)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, c1)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+    dp = ge.gemm_epilogue(A, B, bias, bias_mode="col", tile_n=256, cta_group=2, stream_k=1)
+    torch.cuda.synchronize()
+    o, m = oracle_run(prob, "rc")
+    check_bound(c1.float().cpu().numpy(), o, m, "stream-K")
+    check_bound(dp.float().cpu().numpy(), o, m, "data-parallel")
+
+
+def test_stream_k_library_workspace_via_host_entry():
+    """The host-buffer entry passes no workspace: the library-managed per-device buffer is used."""
+    prob = workloads.make_problem(1024, 1024, 1024, seed=43, kind="smallint", bias_mode="row")
+    Ch = ge.gemm_epilogue_host(prob.A, prob.B, prob.bias, tile_n=256, cta_group=2, stream_k=2)
+    out, _ = oracle_run(prob, "rr")
+    assert np.array_equal(Ch.float().numpy().astype(np.float64), exact_expect(out, torch.float16))
