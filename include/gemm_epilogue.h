@@ -55,12 +55,20 @@ typedef enum { GE_ROW_MAJOR = 0, GE_COL_MAJOR = 1 } ge_layout;
 
 typedef enum { GE_OUT_F16 = 0, GE_OUT_F32 = 1 } ge_out_dtype;
 
-/* The pointwise epilogue (S2 of Listing 1).  BIAS needs a non-NULL bias pointer. */
+/* The pointwise epilogue (S2 of Listing 1), bit flags over the paper's op set "add, subtract,
+ * ReLU, Sigmoid, Tanh": optionally add (or, with GE_EPI_SUB,
+ * subtract) the bias, then at most one activation at the root.  Values 0-3 are the original
+ * ops.  Any op with GE_EPI_BIAS needs a non-NULL bias pointer. */
 typedef enum {
     GE_EPI_NONE = 0,        /* C = A.B                         (Listing 2, plain GEMM)       */
     GE_EPI_BIAS = 1,        /* C = A.B + beta                                               */
     GE_EPI_RELU = 2,        /* C = relu(A.B)                                                 */
-    GE_EPI_BIAS_RELU = 3    /* C = relu(A.B + beta)            (Listing 1, relu_add)         */
+    GE_EPI_BIAS_RELU = 3,   /* C = relu(A.B + beta)            (Listing 1, relu_add)         */
+    GE_EPI_SIGMOID = 4,     /* activation flag: 1 / (1 + exp(-v))                            */
+    GE_EPI_BIAS_SIGMOID = 5,
+    GE_EPI_TANH = 8,        /* activation flag: tanh(v)                                      */
+    GE_EPI_BIAS_TANH = 9,
+    GE_EPI_SUB = 16         /* modifier: subtract the bias (v = A.B - beta); needs GE_EPI_BIAS */
 } ge_epilogue_op;
 
 /* Shape of the bias operand beta (DESIGN.md R-C2). */
@@ -129,6 +137,21 @@ ge_status gemm_epilogue_batched(int64_t batch, int64_t M, int64_t N, int64_t K,
                                 const void* bias, int64_t strideBias,
                                 void* C, int64_t ldc, int64_t strideC,
                                 int32_t op, const ge_options* opt, void* stream);
+
+/*
+ * Sum of matmuls, Listing 4: C = epilogue(prologue-free A.B + P.Q), with
+ * A (M x K1), B (K1 x N), P (M x K2), Q (K2 x N); P takes A's layout and Q takes B's layout
+ * (ldp/ldq their leading dimensions, 0 = packed).  Both products accumulate into the same fp32
+ * Tensor Memory accumulator (one operand stream after the other), then bias/activation are
+ * applied once.  K1 and K2 may differ.  opt->prologue must be NONE.
+ * Alignment/aliasing rules of A/B apply to P/Q.  Asynchronous on `stream`.
+ */
+ge_status gemm2_epilogue(int64_t M, int64_t N, int64_t K1, int64_t K2,
+                         int32_t layoutA, int32_t layoutB,
+                         const void* A, int64_t lda, const void* B, int64_t ldb,
+                         const void* P, int64_t ldp, const void* Q, int64_t ldq,
+                         const void* bias, void* C, int64_t ldc,
+                         int32_t op, const ge_options* opt, void* stream);
 
 /*
  * Host-buffer variant (end-to-end path): same arguments as gemm_epilogue_batched but

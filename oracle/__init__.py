@@ -33,6 +33,7 @@ _lib = None
 LAYOUT = {"row": 0, "col": 1}
 BIAS_MODE = {None: -1, "none": -1, "row": 0, "col": 1, "full": 2}
 PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
+ACT = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}
 
 
 def build(force: bool = False) -> str:
@@ -60,8 +61,11 @@ def _load():
         lib.oracle_f16_decode_array.argtypes = [P, P, I64]
         lib.oracle_f16_encode_array.argtypes = [P, P, I64]
         lib.oracle_gemm_epilogue.restype = I
-        lib.oracle_gemm_epilogue.argtypes = [I64, I64, I64, I, I, P, I64, P, I64, P, I, I64, I, I, P, I,
+        lib.oracle_gemm_epilogue.argtypes = [I64, I64, I64, I, I, P, I64, P, I64, P, I, I, I64, I, I, P, I,
                                              P, I64, P, I64, P, P, I]
+        lib.oracle_gemm2_epilogue.restype = I
+        lib.oracle_gemm2_epilogue.argtypes = [I64, I64, I64, I64, I, I, P, I64, P, I64, P, I64, P, I64, P, I, I, I64,
+                                              I, P, I64, P, I64, P, P, I]
         _lib = lib
     return _lib
 
@@ -106,14 +110,16 @@ def _bits(a) -> np.ndarray:
 def gemm_epilogue(A, B, M: int, N: int, K: int, *, layoutA: str = "row", layoutB: str = "row",
                   lda: Optional[int] = None, ldb: Optional[int] = None,
                   bias=None, bias_mode: Optional[str] = "row", ldbias: int = 0,
-                  relu: bool = True, prologue: Optional[str] = None, scale=None,
+                  relu: bool = True, act: Optional[str] = "default", bias_sub: bool = False,
+                  prologue: Optional[str] = None, scale=None,
                   literal_round: bool = False,
                   rows: Optional[Sequence[int]] = None, cols: Optional[Sequence[int]] = None,
                   nthreads: Optional[int] = None):
     """Evaluate the oracle.  Returns (out, mag) as fp64 arrays of shape (len(rows), len(cols))
     (full M x N when rows/cols are None).  A and B are fp16 storage arrays (flat or 2-D)
     read through the layout index formulas with leading dimensions lda/ldb
-    (default: packed).  ``bias=None`` means no bias term.
+    (default: packed).  ``bias=None`` means no bias term.  The activation is ``act`` (None, "relu",
+    "sigmoid", "tanh"); by default ReLU if ``relu`` else identity.  ``bias_sub`` subtracts the bias.
     """
     lib = _load()
     if lda is None:
@@ -135,10 +141,11 @@ def gemm_epilogue(A, B, M: int, N: int, K: int, *, layoutA: str = "row", layoutB
     nc = N if c is None else c.size
     out = np.empty((nr, nc), dtype=np.float64)
     mag = np.empty((nr, nc), dtype=np.float64)
+    act_code = ACT["relu" if relu else None] if act == "default" else ACT[act]
     rc = lib.oracle_gemm_epilogue(
         M, N, K, LAYOUT[layoutA], LAYOUT[layoutB],
         a.ctypes.data, lda, b.ctypes.data, ldb,
-        bb.ctypes.data if bb is not None else None, bm, ldbias, int(bool(relu)),
+        bb.ctypes.data if bb is not None else None, bm, -1 if bias_sub else 1, ldbias, act_code,
         pro, sc.ctypes.data if sc is not None else None, int(bool(literal_round)),
         r.ctypes.data if r is not None else None, 0 if r is None else r.size,
         c.ctypes.data if c is not None else None, 0 if c is None else c.size,
@@ -151,3 +158,34 @@ def gemm_epilogue(A, B, M: int, N: int, K: int, *, layoutA: str = "row", layoutB
 def bound(out: np.ndarray, mag: np.ndarray) -> np.ndarray:
     """BASELINE.json north_star per-element tolerance: 4e-3*mag + 1e-3*|out|."""
     return 4e-3 * mag + 1e-3 * np.abs(out)
+
+
+def gemm2_epilogue(A, B, P, Q, M: int, N: int, K1: int, K2: int, *, layoutA: str = "row", layoutB: str = "row",
+                   lda=None, ldb=None, ldp=None, ldq=None, bias=None, bias_mode: Optional[str] = "row",
+                   ldbias: int = 0, act: Optional[str] = "relu", bias_sub: bool = False,
+                   rows=None, cols=None, nthreads: Optional[int] = None):
+    """Sum of matmuls (Listing 4): act(A.B + P.Q +- bias).  P, Q use the layouts of A, B."""
+    lib = _load()
+    lda = lda or (K1 if layoutA == "row" else M)
+    ldp = ldp or (K2 if layoutA == "row" else M)
+    ldb = ldb or (N if layoutB == "row" else K1)
+    ldq = ldq or (N if layoutB == "row" else K2)
+    arr = [np.ascontiguousarray(_bits(x)).reshape(-1) for x in (A, B, P, Q)]
+    bm = BIAS_MODE[bias_mode] if bias is not None else -1
+    bb = np.ascontiguousarray(_bits(bias)).reshape(-1) if bias is not None else None
+    r = None if rows is None else np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    c = None if cols is None else np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+    nr = M if r is None else r.size
+    nc = N if c is None else c.size
+    out = np.empty((nr, nc), dtype=np.float64)
+    mag = np.empty((nr, nc), dtype=np.float64)
+    rc = lib.oracle_gemm2_epilogue(
+        M, N, K1, K2, LAYOUT[layoutA], LAYOUT[layoutB], arr[0].ctypes.data, lda, arr[1].ctypes.data, ldb,
+        arr[2].ctypes.data, ldp, arr[3].ctypes.data, ldq, bb.ctypes.data if bb is not None else None, bm,
+        -1 if bias_sub else 1, ldbias, ACT[act],
+        r.ctypes.data if r is not None else None, 0 if r is None else r.size,
+        c.ctypes.data if c is not None else None, 0 if c is None else c.size,
+        out.ctypes.data, mag.ctypes.data, int(nthreads or default_threads()))
+    if rc != 0:
+        raise ValueError(f"oracle_gemm2_epilogue rejected its arguments (rc={rc})")
+    return out, mag

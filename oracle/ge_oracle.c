@@ -12,13 +12,15 @@
  *   Listing 1 (Sec. III "Problem Statement"):
  *       S1: C[i,j] = sum_k A[i,k] * B[k,j]
  *       S2: E[i,j] = relu_add(C[i,j], bias[i,j])   (ReLU at the root)
+ *   generalised to the paper's pointwise op set: add or subtract the
+ *   bias, then ReLU, Sigmoid or Tanh at the root.
  *   Listing 5 (Sec. VII-C "Pointwise Operations in Prologue"):
  *       C[i,j] = sum_k relu(A[i,k]) * B[k,j]
  *   plus the SCALE_K prologue reading of DESIGN.md (R-C12): a'(i,k) = s_k * a(i,k).
  *
  *   a'(i,k)  = a(i,k) | s_k * a(i,k) | max(a(i,k), 0)        (prologue NONE|SCALE_K|RELU)
- *   pre(i,j) = sum_{k<K} a'(i,k) * b(k,j) + beta(i,j)         (beta = 0|bias[j]|bias[i]|bias[i,j])
- *   out(i,j) = relu ? (pre > 0 ? pre : +0) : pre
+ *   pre(i,j) = sum_{k<K} a'(i,k) * b(k,j) +- beta(i,j)        (beta = 0|bias[j]|bias[i]|bias[i,j])
+ *   out(i,j) = act(pre): identity | relu (pre > 0 ? pre : +0) | sigmoid 1/(1+e^-pre) | tanh(pre)
  *   mag(i,j) = sum_{k<K} |a'(i,k) * b(k,j)|                    (scale of the rounding error)
  *
  * The sum runs k = 0, 1, ..., K-1 in that order (Listing 1's loop order).
@@ -103,7 +105,8 @@ typedef struct {
     const uint16_t *A; int64_t lda;
     const uint16_t *B; int64_t ldb;
     const uint16_t *bias; int bias_mode; int64_t ldbias;
-    int relu;
+    int act;                /* 0 identity, 1 relu, 2 sigmoid, 3 tanh */
+    int bias_sign;          /* +1 add, -1 subtract */
     int prologue; const float *scale;
     int literal_round;      /* DESIGN.md R-C3 paper-literal variant: relu(f16(f16(acc)+bias)) */
     /* the evaluated rows I and columns J (the output is out[r*nJ + c] for i=I[r], j=J[c]) */
@@ -146,7 +149,7 @@ static double beta(const job_t *T, int64_t i, int64_t j) {
 }
 
 /* One output element, Listing 1's S1 then S2. */
-static void element(const job_t *T, int64_t r, int64_t c, double *o, double *m) {
+static void element(const job_t *T, int64_t r, int64_t c, double *res, double *m) {
     const double *ar = T->ap + r * T->K;
     const double *bc = T->bt + c * T->K;
     double acc = 0.0, mg = 0.0;
@@ -161,11 +164,18 @@ static void element(const job_t *T, int64_t r, int64_t c, double *o, double *m) 
         /* R-C3 literal reading: accumulator converted to fp16 before the pointwise op
          * (PAPER.md:1109-1112), relu_add on fp16 fragments. */
         double c16 = oracle_f16_to_f64(oracle_f64_to_f16_rne(acc));
-        pre = oracle_f16_to_f64(oracle_f64_to_f16_rne(c16 + beta(T, i, j)));
+        pre = oracle_f16_to_f64(oracle_f64_to_f16_rne(c16 + T->bias_sign * beta(T, i, j)));
     } else {
-        pre = acc + beta(T, i, j);                  /* S2: add */
+        pre = acc + T->bias_sign * beta(T, i, j);   /* S2: add (or subtract) */
     }
-    *o = T->relu ? (pre > 0.0 ? pre : 0.0) : pre;   /* S2: relu at the root */
+    double o;                                       /* S2: activation at the root */
+    switch (T->act) {
+    case 1: o = pre > 0.0 ? pre : 0.0; break;
+    case 2: o = 1.0 / (1.0 + exp(-pre)); break;
+    case 3: o = tanh(pre); break;
+    default: o = pre;
+    }
+    *res = o;
     *m = mg;
 }
 
@@ -207,16 +217,17 @@ static int run_threads(job_t *base, void *(*fn)(void *)) {
  * Evaluate out/mag (fp64, unrounded) on the cross product of rows I x columns J.
  * I == NULL means all M rows (nI ignored), J == NULL all N columns.
  * out[r*nJ + c] is element (I[r], J[c]).  Returns 0, or <0 on bad arguments.
- * bias_mode: -1 none, 0 ROW bias[j], 1 COL bias[i], 2 FULL bias[i*ldbias+j].
- * prologue: 0 none, 1 SCALE_K (scale[k], fp32), 2 RELU.
+ * bias_mode: -1 none, 0 ROW bias[j], 1 COL bias[i], 2 FULL bias[i*ldbias+j]; bias_sign +1/-1.
+ * act: 0 identity, 1 relu, 2 sigmoid, 3 tanh.  prologue: 0 none, 1 SCALE_K (scale[k], fp32), 2 RELU.
  */
 int oracle_gemm_epilogue(int64_t M, int64_t N, int64_t K, int layoutA, int layoutB,
                          const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb,
-                         const uint16_t *bias, int bias_mode, int64_t ldbias, int relu,
+                         const uint16_t *bias, int bias_mode, int bias_sign, int64_t ldbias, int act,
                          int prologue, const float *scale, int literal_round,
                          const int64_t *I, int64_t nI, const int64_t *J, int64_t nJ,
                          double *out, double *mag, int nthreads) {
     if (M < 0 || N < 0 || K < 0) return -1;
+    if (act < 0 || act > 3 || (bias_sign != 1 && bias_sign != -1)) return -1;
     if (bias_mode != OR_BIAS_NONE && !bias) return -1;
     if (prologue == OR_PRO_SCALE_K && !scale) return -1;
     job_t T;
@@ -225,7 +236,7 @@ int oracle_gemm_epilogue(int64_t M, int64_t N, int64_t K, int layoutA, int layou
     T.layoutA = layoutA; T.layoutB = layoutB;
     T.A = A; T.lda = lda; T.B = B; T.ldb = ldb;
     T.bias = bias; T.bias_mode = bias_mode; T.ldbias = ldbias;
-    T.relu = relu; T.prologue = prologue; T.scale = scale;
+    T.act = act; T.bias_sign = bias_sign; T.prologue = prologue; T.scale = scale;
     T.literal_round = literal_round;
     T.I = I; T.nI = I ? nI : M;
     T.J = J; T.nJ = J ? nJ : N;
@@ -250,4 +261,56 @@ void oracle_f16_decode_array(const uint16_t *h, double *out, int64_t n) {
 }
 void oracle_f16_encode_array(const double *x, uint16_t *out, int64_t n) {
     for (int64_t i = 0; i < n; ++i) out[i] = oracle_f64_to_f16_rne(x[i]);
+}
+
+/*
+ * Sum of matmuls, Listing 4 (Sec. VII-B "Matmuls with Pointwise Epilogue"):
+ *     S1: C[i,j] = sum_k A[i,k] B[k,j]      (k < K1)
+ *     S2: R[i,j] = sum_k P[i,k] Q[k,j]      (k < K2)
+ *     S3: Z[i,j] = add(C[i,j], R[i,j])      then the same bias / activation as above
+ * K1 and K2 may differ (the outputs share the shape).  P and Q use the
+ * layouts of A and B.  Evaluated by two plain oracle passes (no bias / activation) and the S3
+ * add, then S2-of-Listing-1 bias and activation; mag = sum|ab| + sum|pq|.
+ */
+int oracle_gemm2_epilogue(int64_t M, int64_t N, int64_t K1, int64_t K2, int layoutA, int layoutB,
+                          const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb,
+                          const uint16_t *P, int64_t ldp, const uint16_t *Q, int64_t ldq,
+                          const uint16_t *bias, int bias_mode, int bias_sign, int64_t ldbias, int act,
+                          const int64_t *I, int64_t nI, const int64_t *J, int64_t nJ,
+                          double *out, double *mag, int nthreads) {
+    const int64_t nr = I ? nI : M, nc = J ? nJ : N;
+    const size_t n = (size_t)(nr * nc);
+    double *c = (double *)malloc((n ? n : 1) * sizeof(double));
+    double *cm = (double *)malloc((n ? n : 1) * sizeof(double));
+    double *r = (double *)malloc((n ? n : 1) * sizeof(double));
+    double *rm = (double *)malloc((n ? n : 1) * sizeof(double));
+    int rc = (c && cm && r && rm) ? 0 : -3;
+    if (rc == 0)
+        rc = oracle_gemm_epilogue(M, N, K1, layoutA, layoutB, A, lda, B, ldb, NULL, OR_BIAS_NONE, 1, 0, 0,
+                                  OR_PRO_NONE, NULL, 0, I, nI, J, nJ, c, cm, nthreads);
+    if (rc == 0)
+        rc = oracle_gemm_epilogue(M, N, K2, layoutA, layoutB, P, ldp, Q, ldq, NULL, OR_BIAS_NONE, 1, 0, 0,
+                                  OR_PRO_NONE, NULL, 0, I, nI, J, nJ, r, rm, nthreads);
+    if (rc == 0) {
+        job_t T;
+        memset(&T, 0, sizeof T);
+        T.bias = bias; T.bias_mode = bias ? bias_mode : OR_BIAS_NONE; T.ldbias = ldbias;
+        for (int64_t a = 0; a < nr; ++a)
+            for (int64_t b = 0; b < nc; ++b) {
+                const size_t x = (size_t)(a * nc + b);
+                const int64_t i = I ? I[a] : a, j = J ? J[b] : b;
+                const double pre = (c[x] + r[x]) + bias_sign * beta(&T, i, j);       /* S3, then bias */
+                double o;
+                switch (act) {
+                case 1: o = pre > 0.0 ? pre : 0.0; break;
+                case 2: o = 1.0 / (1.0 + exp(-pre)); break;
+                case 3: o = tanh(pre); break;
+                default: o = pre;
+                }
+                out[x] = o;
+                mag[x] = cm[x] + rm[x];
+            }
+    }
+    free(c); free(cm); free(r); free(rm);
+    return rc;
 }

@@ -21,7 +21,7 @@ from typing import Optional
 
 import torch
 
-__all__ = ["gemm_epilogue", "gemm_epilogue_batched", "gemm_epilogue_host", "GEError", "plan", "validate_args",
+__all__ = ["gemm_epilogue", "gemm2_epilogue", "gemm_epilogue_batched", "gemm_epilogue_host", "GEError", "plan", "validate_args",
            "launch_count", "version", "library_path", "load_library", "layout_of", "Status"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -38,7 +38,8 @@ class Status:
     CUDA = 5
 
 
-EPI = {"none": 0, "bias": 1, "relu": 2, "bias_relu": 3}
+EPI = {"none": 0, "bias": 1, "relu": 2, "bias_relu": 3, "sigmoid": 4, "bias_sigmoid": 5, "tanh": 8, "bias_tanh": 9,
+       "sub_bias": 17, "sub_bias_relu": 19, "sub_bias_sigmoid": 21, "sub_bias_tanh": 25}
 BIAS_MODE = {"row": 0, "col": 1, "full": 2}
 PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
 
@@ -76,6 +77,8 @@ def load_library():
     batched = [I64, I64, I64, I64, I32, I32, P, I64, I64, P, I64, I64, P, I64, P, I64, I64, I32, OPT]
     lib.gemm_epilogue_batched.restype = I32
     lib.gemm_epilogue_batched.argtypes = batched + [P]
+    lib.gemm2_epilogue.restype = I32
+    lib.gemm2_epilogue.argtypes = [I64, I64, I64, I64, I32, I32, P, I64, P, I64, P, I64, P, I64, P, P, I64, I32, OPT, P]
     lib.gemm_epilogue_host.restype = I32
     lib.gemm_epilogue_host.argtypes = batched + [P]
     lib.ge_validate.restype = I32
@@ -185,8 +188,9 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     """C = relu_add(prologue(A) @ B, bias) on the current CUDA device (fp16 in, fp32 accumulate).
 
     A: (M, K) fp16, B: (K, N) fp16, row- or column-major views.  bias: (N,) for bias_mode "row",
-    (M,) for "col", (M, ldbias>=N) row-major for "full".  op in {"none","bias","relu","bias_relu"}
-    (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32) or "relu".
+    (M,) for "col", (M, ldbias>=N) row-major for "full".  op in {"none", "bias", "relu", "bias_relu",
+    "sigmoid", "bias_sigmoid", "tanh", "bias_tanh", "sub_bias", "sub_bias_relu", "sub_bias_sigmoid",
+    "sub_bias_tanh"} (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32) or "relu".
     Returns C (M, N) row-major in out_dtype (fp16 or fp32), asynchronously on the current stream.
     """
     lib = load_library()
@@ -209,6 +213,38 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
                            bias.data_ptr() if bias is not None else None, out.data_ptr(), max(out.stride(0), N, 1),
                            _op(op, bias), ctypes.byref(o), sh)
+    _check(st)
+    return out
+
+
+def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.Tensor,
+                   bias: Optional[torch.Tensor] = None, *, op: Optional[str] = None, bias_mode: str = "row",
+                   out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
+                   cta_group: int = 0, stream_k: int = 0, stream=None) -> torch.Tensor:
+    """Sum of matmuls (Listing 4): C = epilogue(A @ B + P @ Q) in one kernel, one TMEM
+    accumulator.  A (M, K1), B (K1, N), P (M, K2), Q (K2, N); P must share A's layout (row/col
+    major) and Q B's."""
+    lib = load_library()
+    M, K1 = A.shape
+    N = B.shape[1]
+    K2 = P.shape[1]
+    if B.shape[0] != K1 or P.shape[0] != M or Q.shape != (K2, N):
+        raise ValueError("shapes of A.B and P.Q disagree")
+    la, lda = layout_of(A)
+    lb, ldb = layout_of(B)
+    lp, ldp = layout_of(P)
+    lq, ldq = layout_of(Q)
+    if lp != la or lq != lb:
+        raise ValueError("P must have A's layout and Q must have B's layout")
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=A.device)
+    ldbias, _ = _bias_ld(bias, bias_mode)
+    sh = _stream(stream)
+    o = _options(bias_mode, ldbias, None, None, out.dtype, tile_n, cta_group, stream_k,
+                 _workspace(A.device, sh) if stream_k != 1 else None)
+    st = lib.gemm2_epilogue(M, N, K1, K2, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb, P.data_ptr(), ldp,
+                            Q.data_ptr(), ldq, bias.data_ptr() if bias is not None else None, out.data_ptr(),
+                            max(out.stride(0), N, 1), _op(op, bias), ctypes.byref(o), sh)
     _check(st)
     return out
 

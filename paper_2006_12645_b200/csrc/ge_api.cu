@@ -77,6 +77,12 @@ struct Args {
     int64_t ldc, sC;
     int32_t op;
     ge_options o;
+    // second matmul of a sum of matmuls (gemm2_epilogue, Listing 4): P (layout of A), Q (of B)
+    int64_t K2 = 0;
+    const void* P = nullptr;
+    int64_t ldp = 0;
+    const void* Q = nullptr;
+    int64_t ldq = 0;
 };
 
 int64_t extent_bytes(int64_t batch, int64_t outer, int64_t inner, int64_t ld, int64_t stride, int es) {
@@ -90,8 +96,18 @@ bool overlap(const void* a, int64_t na, const void* b, int64_t nb) {
     return x < y + static_cast<uintptr_t>(nb) && y < x + static_cast<uintptr_t>(na);
 }
 
-bool has_bias(int32_t op) { return op == GE_EPI_BIAS || op == GE_EPI_BIAS_RELU; }
-bool has_relu(int32_t op) { return op == GE_EPI_RELU || op == GE_EPI_BIAS_RELU; }
+// op bit flags (include/gemm_epilogue.h): bit 0 bias, bit 1 ReLU, bit 2 Sigmoid, bit 3 Tanh,
+// bit 4 subtract the bias; at most one activation, subtraction only with a bias.
+bool op_valid(int32_t op) {
+    if (op < 0 || op > 31) return false;
+    const int acts = ((op >> 1) & 1) + ((op >> 2) & 1) + ((op >> 3) & 1);
+    return acts <= 1 && (!(op & GE_EPI_SUB) || (op & GE_EPI_BIAS));
+}
+bool has_bias(int32_t op) { return (op & GE_EPI_BIAS) != 0; }
+int act_of(int32_t op) {
+    return (op & GE_EPI_RELU) ? ge::ACT_RELU : (op & GE_EPI_SIGMOID) ? ge::ACT_SIGMOID
+                                                  : (op & GE_EPI_TANH) ? ge::ACT_TANH : ge::ACT_NONE;
+}
 
 // Normalises ld/stride defaults in place and checks everything that can be checked on the host.
 ge_status validate(Args& a) {
@@ -102,7 +118,7 @@ ge_status validate(Args& a) {
         return fail(GE_ERR_INVALID_VALUE, "size exceeds 2^31-1");
     if ((a.la != GE_ROW_MAJOR && a.la != GE_COL_MAJOR) || (a.lb != GE_ROW_MAJOR && a.lb != GE_COL_MAJOR))
         return fail(GE_ERR_INVALID_VALUE, "layout must be GE_ROW_MAJOR or GE_COL_MAJOR");
-    if (a.op < GE_EPI_NONE || a.op > GE_EPI_BIAS_RELU) return fail(GE_ERR_INVALID_VALUE, "bad epilogue op");
+    if (!op_valid(a.op)) return fail(GE_ERR_INVALID_VALUE, "bad epilogue op (see ge_epilogue_op flags)");
     const ge_options& o = a.o;
     if (o.bias_mode < GE_BIAS_ROW || o.bias_mode > GE_BIAS_FULL) return fail(GE_ERR_INVALID_VALUE, "bad bias_mode");
     if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_RELU) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
@@ -142,6 +158,25 @@ ge_status validate(Args& a) {
     if (has_bias(a.op) && !a.bias) return fail(GE_ERR_INVALID_VALUE, "bias is NULL but the op adds a bias");
     if (a.o.prologue == GE_PRO_SCALE_K && a.K > 0 && !a.o.prologue_scale)
         return fail(GE_ERR_INVALID_VALUE, "prologue_scale is NULL for GE_PRO_SCALE_K");
+    if (a.K2 < 0 || a.K2 > kMaxDim) return fail(GE_ERR_INVALID_VALUE, "K2 out of range");
+    if (a.K2 > 0) {
+        if (a.o.prologue != GE_PRO_NONE)
+            return fail(GE_ERR_INVALID_VALUE, "the prologue is not supported with a sum of matmuls");
+        const int64_t minldp = arow ? a.K2 : a.M, minldq = brow ? a.N : a.K2;
+        if (a.ldp == 0) a.ldp = std::max<int64_t>(minldp, 1);
+        if (a.ldq == 0) a.ldq = std::max<int64_t>(minldq, 1);
+        if (a.ldp < minldp || a.ldq < minldq) return fail(GE_ERR_INVALID_VALUE, "ldp or ldq too small");
+        if (!a.P || !a.Q) return fail(GE_ERR_INVALID_VALUE, "P or Q is NULL");
+        if ((reinterpret_cast<uintptr_t>(a.P) & 15) || (reinterpret_cast<uintptr_t>(a.Q) & 15))
+            return fail(GE_ERR_MISALIGNED, "P and Q must be 16-byte aligned (TMA)");
+        if ((a.ldp * 2) % 16 || (a.ldq * 2) % 16)
+            return fail(GE_ERR_MISALIGNED, "ldp and ldq must be multiples of 8 elements (16 bytes, TMA)");
+        const int es2 = a.o.out_dtype == GE_OUT_F32 ? 4 : 2;
+        const int64_t nC2 = extent_bytes(a.batch, a.M, a.N, a.ldc, a.sC, es2);
+        if (overlap(a.C, nC2, a.P, extent_bytes(1, arow ? a.M : a.K2, arow ? a.K2 : a.M, a.ldp, 0, 2)) ||
+            overlap(a.C, nC2, a.Q, extent_bytes(1, brow ? a.K2 : a.N, brow ? a.N : a.K2, a.ldq, 0, 2)))
+            return fail(GE_ERR_ALIASING, "C overlaps P or Q");
+    }
     if (a.K > 0) {
         if ((reinterpret_cast<uintptr_t>(a.A) & 15) || (reinterpret_cast<uintptr_t>(a.B) & 15))
             return fail(GE_ERR_MISALIGNED, "A and B must be 16-byte aligned (TMA)");
@@ -201,7 +236,8 @@ Plan make_plan(const Args& a, int sms) {
     Plan best{};
     double best_cost = 0;
     const int cands[6][2] = {{512, 2}, {256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
-    const int64_t nkb = cdiv(a.K, 64);
+    const int64_t nkb = cdiv(a.K, 64) + cdiv(a.K2, 64);
+    const int64_t Ktot = a.K + a.K2;
     for (const auto& c : cands) {
         const int bn = c[0], cg = c[1];
         if (a.o.tile_n && a.o.tile_n != bn) continue;
@@ -212,7 +248,7 @@ Plan make_plan(const Args& a, int sms) {
         if (a.M <= 64 && !a.o.tile_n && !a.o.cta_group && !(bn == 128 && cg == 1)) continue;
         const int64_t tiles = a.batch * cdiv(a.M, 128 * cg) * cdiv(a.N, bn);
         const int64_t conc = std::max(1, sms / cg);
-        const double kk = static_cast<double>(std::max<int64_t>(a.K, 64)) + (bn == 512 ? kExposedK : 0.0);
+        const double kk = static_cast<double>(std::max<int64_t>(Ktot, 64)) + (bn == 512 ? kExposedK : 0.0);
         double eff = config_eff(bn, cg);
         // The prologue transform rewrites each 16 KB A stage in smem: configurations with less MMA
         // time per stage than 256 x 512 pair tiles become shared-memory bound.
@@ -376,6 +412,16 @@ ge_status launch(Args& a, cudaStream_t st) {
         else ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.N, a.K, a.batch, a.ldb, a.sB, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for B");
     }
+    if (a.K2 > 0) {
+        bool ok;
+        if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.K2, a.M, 1, a.ldp, 0, 64, 128);
+        else ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.M, a.K2, 1, a.ldp, 0, 64, 64);
+        if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for P");
+        const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg);
+        if (!b_mn) ok = encode3d(&maps.q, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.Q, a.K2, a.N, 1, a.ldq, 0, 64, brows);
+        else ok = encode3d(&maps.q, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.Q, a.N, a.K2, 1, a.ldq, 0, 64, 64);
+        if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for Q");
+    }
     const bool c_tma = (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && ((a.ldc * es) % 16 == 0) &&
                        (a.batch == 1 || (a.sC * es) % 16 == 0);
     if (c_tma) {
@@ -391,7 +437,8 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.batch = static_cast<int>(a.batch);
     p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg));
     p.num_n_tiles = static_cast<int>(cdiv(a.N, pl.bn));
-    p.num_k_blocks = static_cast<int>(cdiv(a.K, ge::kBK));
+    p.num_k_blocks1 = static_cast<int>(cdiv(a.K, ge::kBK));
+    p.num_k_blocks = p.num_k_blocks1 + static_cast<int>(cdiv(a.K2, ge::kBK));
     p.group_m = group_m_for(pl, a, sms);
     {
         static int hints[3] = {-1, -1, -1};
@@ -411,7 +458,8 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.stride_bias = a.sBias;
     p.bias_vec = p.bias && (reinterpret_cast<uintptr_t>(p.bias) % 16 == 0) && (a.sBias % 8 == 0) &&
                  (a.o.bias_mode != GE_BIAS_FULL || a.o.ldbias % 8 == 0);
-    p.relu = has_relu(a.op) ? 1 : 0;
+    p.act = act_of(a.op);
+    p.bias_sign = (a.op & GE_EPI_SUB) ? -1.0f : 1.0f;
     p.scale = a.o.prologue == GE_PRO_SCALE_K ? a.o.prologue_scale : nullptr;
     p.prologue = a.o.prologue;
     p.scale_vec = p.scale && (reinterpret_cast<uintptr_t>(p.scale) % 16 == 0);
@@ -517,6 +565,20 @@ ge_status gemm_epilogue_batched(int64_t batch, int64_t M, int64_t N, int64_t K, 
                                 int64_t strideC, int32_t op, const ge_options* opt, void* stream) {
     Args a = make_args(batch, M, N, K, layoutA, layoutB, A, lda, strideA, B, ldb, strideB, bias, strideBias, C, ldc,
                        strideC, op, opt);
+    g_detail.clear();
+    return launch(a, static_cast<cudaStream_t>(stream));
+}
+
+ge_status gemm2_epilogue(int64_t M, int64_t N, int64_t K1, int64_t K2, int32_t layoutA, int32_t layoutB,
+                         const void* A, int64_t lda, const void* B, int64_t ldb, const void* P, int64_t ldp,
+                         const void* Q, int64_t ldq, const void* bias, void* C, int64_t ldc, int32_t op,
+                         const ge_options* opt, void* stream) {
+    Args a = make_args(1, M, N, K1, layoutA, layoutB, A, lda, 0, B, ldb, 0, bias, 0, C, ldc, 0, op, opt);
+    a.K2 = K2;
+    a.P = P;
+    a.ldp = ldp;
+    a.Q = Q;
+    a.ldq = ldq;
     g_detail.clear();
     return launch(a, static_cast<cudaStream_t>(stream));
 }

@@ -41,10 +41,12 @@ constexpr int kStagingSetBytes = 16384; // one staging buffer per epilogue warp:
 
 enum : int { BIAS_NONE = -1, BIAS_ROW = 0, BIAS_COL = 1, BIAS_FULL = 2 };
 enum : int { PRO_NONE = 0, PRO_SCALE_K = 1, PRO_RELU = 2 };
+enum : int { ACT_NONE = 0, ACT_RELU = 1, ACT_SIGMOID = 2, ACT_TANH = 3 };
 
 struct Params {
     int M, N, K, batch;
     int num_m_tiles, num_n_tiles, num_k_blocks;
+    int num_k_blocks1;              // k-blocks of A.B; the rest come from P.Q (sum of matmuls, Listing 4)
     int group_m;                    // raster group (m-tiles per group) for L2 locality
     long long num_tiles;
     // epilogue
@@ -52,7 +54,8 @@ struct Params {
     int bias_mode;                  // BIAS_*
     int bias_vec;                   // 16-B vector loads of bias are legal
     long long ldbias, stride_bias;
-    int relu;
+    int act;                        // ACT_* applied at the root of the epilogue
+    float bias_sign;                // +1 add, -1 subtract the bias
     // prologue
     const float* scale;
     int prologue;                   // PRO_*
@@ -189,10 +192,19 @@ struct WorkSeq {
     __device__ __forceinline__ bool has_units(int c) const { return range_begin(c + 1) > range_begin(c); }
 };
 
-// fp32 epilogue value: v = acc + beta, then relu (y = v > 0 ? v : +0, DESIGN.md R-C5).
-__device__ __forceinline__ float epi(float acc, float beta, int relu) {
-    const float v = acc + beta;
-    return relu ? (v > 0.0f ? v : 0.0f) : v;
+// Activation at the root of the pointwise epilogue, fp32, IEEE
+// library functions (no fast math, DESIGN.md R-C7).  ReLU: y = v > 0 ? v : +0 (DESIGN.md R-C5).
+__device__ __forceinline__ void activate(float* f, int n, int act) {
+    if (act == ACT_RELU) {
+#pragma unroll
+        for (int e = 0; e < n; ++e) f[e] = f[e] > 0.0f ? f[e] : 0.0f;
+    } else if (act == ACT_SIGMOID) {
+#pragma unroll
+        for (int e = 0; e < n; ++e) f[e] = 1.0f / (1.0f + expf(-f[e]));
+    } else if (act == ACT_TANH) {
+#pragma unroll
+        for (int e = 0; e < n; ++e) f[e] = tanhf(f[e]);
+    }
 }
 
 // Epilogue warps: 8 (two per TMEM lane quarter) for the fp16 fast path, 4 when the fp32 staging
@@ -205,7 +217,8 @@ __host__ __device__ constexpr int kernel_threads(bool out_f32, bool pro) {
 template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG>
 __global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO), 1)
 ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                const __grid_constant__ CUtensorMap tmap_c, const Params p) {
+                const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_p,
+                const __grid_constant__ CUtensorMap tmap_q, const Params p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     using C_ = Cfg<BN, CG>;
     constexpr int S = C_::kStages;
@@ -240,6 +253,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmap_a);
         ptx::tma_prefetch(&tmap_b);
+        if (p.num_k_blocks1 < p.num_k_blocks) {
+            ptx::tma_prefetch(&tmap_p);
+            ptx::tma_prefetch(&tmap_q);
+        }
         if (p.c_tma) ptx::tma_prefetch(&tmap_c);
     }
     if (warp == 1 && lane == 0) {
@@ -283,7 +300,11 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                     ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg ? &dbg[DBG_PROD_EMPTY] : nullptr);
-                    const int k0 = kb * kBK;
+                    // sum of matmuls (Listing 4): k-blocks past A.B's come from P.Q, same accumulator
+                    const bool second = kb >= p.num_k_blocks1;
+                    const CUtensorMap* map_a = second ? &tmap_p : &tmap_a;
+                    const CUtensorMap* map_b = second ? &tmap_q : &tmap_b;
+                    const int k0 = (second ? kb - p.num_k_blocks1 : kb) * kBK;
                     uint8_t* sa = smem_a + s * C_::kAStage;
                     uint8_t* sb = smem_b + s * C_::kBStage;
                     if (p.dbg_noload && (wi != 0 || kb >= S)) {
@@ -306,9 +327,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     };
                     if constexpr (A_MN) {
 #pragma unroll
-                        for (int i = 0; i < kRowsPerCta / 64; ++i) load(sa + i * 8192, &tmap_a, m0 + i * 64, k0, pol_a);
+                        for (int i = 0; i < kRowsPerCta / 64; ++i) load(sa + i * 8192, map_a, m0 + i * 64, k0, pol_a);
                     } else {
-                        load(sa, &tmap_a, k0, m0, pol_a);
+                        load(sa, map_a, k0, m0, pol_a);
                     }
 #pragma unroll
                     for (int h = 0; h < NH; ++h) {
@@ -317,9 +338,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if constexpr (B_MN) {
 #pragma unroll
                             for (int i = 0; i < C_::kBBlockRows / 64; ++i)
-                                load(sbh + i * 8192, &tmap_b, nh + i * 64, k0, pol_b);
+                                load(sbh + i * 8192, map_b, nh + i * 64, k0, pol_b);
                         } else {
-                            load(sbh, &tmap_b, k0, nh, pol_b);
+                            load(sbh, map_b, k0, nh, pol_b);
                         }
                     }
                     if (++s == S) { s = 0; phase ^= 1; }
@@ -343,47 +364,94 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
                 const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
-                    ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
-                    ptx::tc_fence_after();
-                    const uint32_t sa = a_base + s * C_::kAStage;
-                    const uint32_t sb = b_base + s * C_::kBStage;
-                    // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
-                    // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
-                    // SBO = next 8-row K group (1024 B).
-                    auto mma_one = [&](int h, int k) {
-                        const uint32_t sbh = sb + h * C_::kBBlockBytes;
-                        const uint64_t ad = A_MN ? ptx::make_sw128_desc(sa + k * 2048, 8192, 1024)
-                                                 : ptx::make_sw128_desc(sa + k * 32, 0, 1024);
-                        const uint64_t bd = B_MN ? ptx::make_sw128_desc(sbh + k * 2048, 8192, 1024)
-                                                 : ptx::make_sw128_desc(sbh + k * 32, 0, 1024);
-                        ptx::mma_f16_elect<CG>(d_tmem + h * C_::kUmmaN, ad, bd, IDESC, (kb != pc.kb0) || k != 0);
-                    };
-                    if (kb == pc.kb0) {
-                        // first k-block of a tile: start on accumulator half 0 as soon as the
-                        // epilogue has drained it, then wait for half 1
+                // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
+                // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
+                // SBO = next 8-row K group (1024 B).
+                auto mma_one = [&](int stage, int kb, int h, int k) {
+                    const uint32_t sa = a_base + stage * C_::kAStage;
+                    const uint32_t sbh = b_base + stage * C_::kBStage + h * C_::kBBlockBytes;
+                    const uint64_t ad = A_MN ? ptx::make_sw128_desc(sa + k * 2048, 8192, 1024)
+                                             : ptx::make_sw128_desc(sa + k * 32, 0, 1024);
+                    const uint64_t bd = B_MN ? ptx::make_sw128_desc(sbh + k * 2048, 8192, 1024)
+                                             : ptx::make_sw128_desc(sbh + k * 32, 0, 1024);
+                    ptx::mma_f16_elect<CG>(d_tmem + h * C_::kUmmaN, ad, bd, IDESC, (kb != pc.kb0) || k != 0);
+                };
+                if constexpr (NH == 2) {
+                    // Single 512-column accumulator, drained half by half by the epilogue.  Half-0
+                    // MMAs start as soon as half 0 is drained; while half 1 is still being drained the
+                    // half-1 MMAs of the first stages are deferred (their stages stay held) and caught
+                    // up in order once it is free, so the drain overlaps up to S stages of MMA work.
+                    int npend = 0, s_pend = s;
+                    bool h1_free = false;
+                    for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
+                        if (npend == S) {          // every stage is held: block until half 1 is drained
+                            ptx::mbar_wait_timed(&tempty_bar[1], acc_phase ^ 1,
+                                                 (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                            h1_free = true;
+                        }
+                        if (h1_free && npend > 0) {
+                            ptx::tc_fence_after();
+                            for (int i = 0; i < npend; ++i) {
+                                const int st = (s_pend + i) % S;
 #pragma unroll
-                        for (int h = 0; h < NH; ++h) {
-                            ptx::mbar_wait_timed(&tempty_bar[acc * NH + h], acc_phase ^ 1,
+                                for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(st, pc.kb0 + i, 1, k);
+                                ptx::mma_commit_elect<CG>(&empty_bar[st]);
+                            }
+                            npend = 0;
+                        }
+                        ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
+                        ptx::tc_fence_after();
+                        if (kb == pc.kb0) {
+                            ptx::mbar_wait_timed(&tempty_bar[0], acc_phase ^ 1,
                                                  (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
                             ptx::tc_fence_after();
-#pragma unroll
-                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(h, k);
+                            h1_free = ptx::mbar_test(&tempty_bar[1], acc_phase ^ 1);
+                            if (h1_free) ptx::tc_fence_after();
+                            s_pend = s;
                         }
-                    } else if (p.dbg_flags & 2) {
+                        if (h1_free) {
 #pragma unroll
-                        for (int h = 0; h < NH; ++h)
+                            for (int k = 0; k < kBK / kUmmaK; ++k) {
+                                mma_one(s, kb, 0, k);
+                                mma_one(s, kb, 1, k);
+                            }
+                            ptx::mma_commit_elect<CG>(&empty_bar[s]);
+                        } else {
 #pragma unroll
-                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(h, k);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < kBK / kUmmaK; ++k)
-#pragma unroll
-                            for (int h = 0; h < NH; ++h) mma_one(h, k);
+                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(s, kb, 0, k);
+                            ++npend;
+                            h1_free = ptx::mbar_test(&tempty_bar[1], acc_phase ^ 1);
+                        }
+                        if (++s == S) { s = 0; phase ^= 1; }
                     }
-                    ptx::mma_commit_elect<CG>(&empty_bar[s]);    // smem slot free once these MMAs finish
-                    if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
-                    if (++s == S) { s = 0; phase ^= 1; }
+                    if (npend > 0) {               // short tile: catch up before signalling the epilogue
+                        ptx::mbar_wait_timed(&tempty_bar[1], acc_phase ^ 1,
+                                             (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                        ptx::tc_fence_after();
+                        for (int i = 0; i < npend; ++i) {
+                            const int st = (s_pend + i) % S;
+#pragma unroll
+                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(st, pc.kb0 + i, 1, k);
+                            ptx::mma_commit_elect<CG>(&empty_bar[st]);
+                        }
+                    }
+                    ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
+                } else {
+                    for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
+                        ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
+                        ptx::tc_fence_after();
+                        if (kb == pc.kb0) {
+                            // first k-block of a tile: the epilogue must have drained this buffer
+                            ptx::mbar_wait_timed(&tempty_bar[acc], acc_phase ^ 1,
+                                                 (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                            ptx::tc_fence_after();
+                        }
+#pragma unroll
+                        for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(s, kb, 0, k);
+                        ptx::mma_commit_elect<CG>(&empty_bar[s]);    // smem slot free once these MMAs finish
+                        if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
+                        if (++s == S) { s = 0; phase ^= 1; }
+                    }
                 }
             }
         }
@@ -464,6 +532,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // S2 of Listing 1: v = acc + beta, relu, one RNE conversion; packed into NWORD words
             auto compute = [&](const int c, const uint32_t* v, uint32_t* w) {
                 const int col0 = nt * BN + c * W;
+                const float bsg = p.bias_sign;
                 float f[W];
 #pragma unroll
                 for (int e = 0; e < W; ++e) f[e] = __uint_as_float(v[e]);
@@ -476,8 +545,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float2 bf = __half22float2(h2[e]);
-                            f[g * 8 + 2 * e] = epi(f[g * 8 + 2 * e], bf.x, p.relu);
-                            f[g * 8 + 2 * e + 1] = epi(f[g * 8 + 2 * e + 1], bf.y, p.relu);
+                            f[g * 8 + 2 * e] += bsg * bf.x;
+                            f[g * 8 + 2 * e + 1] += bsg * bf.y;
                         }
                     }
                 } else if (p.bias_mode == BIAS_FULL) {
@@ -491,8 +560,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 const float2 bf = __half22float2(h2[e]);
-                                f[g * 8 + 2 * e] = epi(f[g * 8 + 2 * e], bf.x, p.relu);
-                                f[g * 8 + 2 * e + 1] = epi(f[g * 8 + 2 * e + 1], bf.y, p.relu);
+                                f[g * 8 + 2 * e] += bsg * bf.x;
+                                f[g * 8 + 2 * e + 1] += bsg * bf.y;
                             }
                         }
                     } else {
@@ -500,14 +569,15 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         for (int e = 0; e < W; ++e) {
                             const int col = col0 + e;
                             const float bv = (col < p.N && in_row) ? __half2float(bsrc[col]) : 0.0f;
-                            f[e] = epi(f[e], bv, p.relu);
+                            f[e] += bsg * bv;
                         }
                     }
                 } else {
                     const float bv = (p.bias_mode == BIAS_COL) ? beta_col : 0.0f;
 #pragma unroll
-                    for (int e = 0; e < W; ++e) f[e] = epi(f[e], bv, p.relu);
+                    for (int e = 0; e < W; ++e) f[e] += bsg * bv;
                 }
+                activate(f, W, p.act);
                 if constexpr (OUT_F32) {
 #pragma unroll
                     for (int e = 0; e < W; ++e) w[e] = __float_as_uint(f[e]);

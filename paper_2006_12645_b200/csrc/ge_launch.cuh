@@ -9,7 +9,7 @@
 namespace ge {
 
 struct Maps {
-    CUtensorMap a, b, c;
+    CUtensorMap a, b, c, p, q;      // p, q: second matmul of a sum of matmuls (unused otherwise)
 };
 
 // Smem bytes the (BN, CG) configuration requests (host and device agree through Cfg).
@@ -38,7 +38,7 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.c, p);
+    return cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.c, m.p, m.q, p);
 }
 
 // Dispatch over the 16 (A_MN, B_MN, OUT_F32, PRO) variants of one (BN, CG) configuration.

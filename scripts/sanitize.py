@@ -1,0 +1,19 @@
+"""Dev: small shapes through every kernel configuration, for compute-sanitizer runs."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2006_12645_b200 as ge
+torch.manual_seed(0)
+for (M, N, K) in [(300, 520, 200), (129, 257, 65)]:
+    up8 = lambda v: (v + 7) // 8 * 8                       # TMA: 16-byte row pitch
+    A = torch.randn(M, up8(K), device="cuda", dtype=torch.float16)[:, :K]
+    B = torch.randn(N, up8(K), device="cuda", dtype=torch.float16)[:, :K].t()
+    bias = torch.randn(N, device="cuda", dtype=torch.float16)
+    scale = torch.rand(K, device="cuda") + 0.5
+    for bn, cg in [(512, 2), (256, 2), (256, 1), (128, 2), (128, 1), (64, 1)]:
+        for sk in (1, 2):
+            ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, stream_k=sk)
+        ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, prologue="scale_k", scale=scale, stream_k=1)
+        ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, out_dtype=torch.float32, stream_k=1)
+torch.cuda.synchronize()
+print("sanitize workload done")

@@ -257,3 +257,53 @@ def test_stream_k_library_workspace_via_host_entry():
     Ch = ge.gemm_epilogue_host(prob.A, prob.B, prob.bias, tile_n=256, cta_group=2, stream_k=2)
     out, _ = oracle_run(prob, "rr")
     assert np.array_equal(Ch.float().numpy().astype(np.float64), exact_expect(out, torch.float16))
+
+
+# ------------------------------------------------------------------ the paper's pointwise op set
+OPS = {"sigmoid": (None, False), "bias_sigmoid": ("sigmoid", False), "tanh": (None, False),
+       "bias_tanh": ("tanh", False), "sub_bias": (None, True), "sub_bias_relu": ("relu", True),
+       "sub_bias_sigmoid": ("sigmoid", True), "sub_bias_tanh": ("tanh", True)}
+
+
+@pytest.mark.parametrize("op", sorted(OPS))
+@pytest.mark.parametrize("tile_n,cg", [(512, 2), (256, 2), (64, 1)])
+def test_pointwise_ops(op, tile_n, cg):
+    """add / subtract bias then ReLU / Sigmoid / Tanh at the root,
+    within the north_star bound (sigmoid' <= 1/4 and tanh' <= 1 do not amplify the pre-activation
+    error); bias-subtracting identity ops stay bitwise exact on small integers."""
+    act = "sigmoid" if "sigmoid" in op else "tanh" if "tanh" in op else "relu" if "relu" in op else None
+    use_bias = "bias" in op
+    sub = op.startswith("sub")
+    for kind in ("uniform", "smallint"):
+        prob = workloads.make_problem(300, 520, 200, seed=44, kind=kind, bias_mode="row")
+        if not use_bias:
+            prob = workloads.Problem(prob.M, prob.N, prob.K, prob.A, prob.B, None, None,
+                                     {"bias_mode": None, "prologue": None})
+        got = run_gpu(prob, "rc", op=op, tile_n=tile_n, cta_group=cg)
+        out, mag = oracle_run(prob, "rc", act=act, bias_sub=sub)
+        if kind == "smallint" and act in (None, "relu"):
+            assert np.array_equal(got, exact_expect(out, torch.float16)), op
+        else:
+            check_bound(got, out, mag, op)
+
+
+# ------------------------------------------------------------------ sum of matmuls (Listing 4)
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+@pytest.mark.parametrize("tile_n,cg", [(512, 2), (256, 2), (128, 1)])
+def test_gemm2_sum_of_matmuls(layouts, tile_n, cg):
+    """Z = relu(A.B + P.Q + bias) in one kernel, K1 != K2 with K tails:
+    bitwise exact on small integers, within the bound on uniform data."""
+    M, N, K1, K2 = 300, 520, 200, 136
+    for kind in ("smallint", "uniform"):
+        p1 = workloads.make_problem(M, N, K1, seed=45, kind=kind, bias_mode="row")
+        p2 = workloads.make_problem(M, N, K2, seed=46, kind=kind, bias_mode=None)
+        A, B = dev_operands(p1, layouts)
+        P, Q = dev_operands(p2, layouts)
+        C = ge.gemm2_epilogue(A, B, P, Q, p1.bias.cuda(), tile_n=tile_n, cta_group=cg)
+        torch.cuda.synchronize()
+        got = C.float().cpu().numpy().astype(np.float64)
+        out, mag = oracle.gemm2_epilogue(p1.A, p1.B, p2.A, p2.B, M, N, K1, K2, bias=p1.bias, act="relu")
+        if kind == "smallint":
+            assert np.array_equal(got, exact_expect(out, torch.float16))
+        else:
+            check_bound(got, out, mag, "gemm2")

@@ -319,3 +319,99 @@ def test_bad_arguments_rejected():
     with pytest.raises(ValueError):
         oracle.gemm_epilogue(np.zeros(4, np.uint16), np.zeros(4, np.uint16), 2, 2, 2, bias=None,
                              rows=[5], cols=[0])
+
+
+# ---------------------------------------------------------------- the paper's pointwise op set
+# add, subtract, ReLU, Sigmoid, Tanh.  Pinned by special values and
+# identities the mathematics fixes (not by retyping the formulas).
+def _prob_nobias(M=48, N=40, K=32, seed=60):
+    return workloads.make_problem(M, N, K, seed=seed, bias_mode=None)
+
+
+def _run(prob, A=None, act=None, bias=None, bias_sub=False, layouts="rc"):
+    p = workloads.Problem(prob.M, prob.N, prob.K, prob.A if A is None else A, prob.B, bias, None,
+                          {"bias_mode": "row" if bias is not None else None, "prologue": None})
+    As, lda = workloads.store(p.A, layouts[0])
+    Bs, ldb = workloads.store(p.B, layouts[1])
+    return oracle.gemm_epilogue(As, Bs, p.M, p.N, p.K, layoutA="row" if layouts[0] == "r" else "col",
+                                layoutB="row" if layouts[1] == "r" else "col", lda=lda, ldb=ldb,
+                                bias=bias, bias_mode="row", act=act, bias_sub=bias_sub)[0]
+
+
+def test_sigmoid_tanh_at_zero():
+    """sigma(0) = 1/2 and tanh(0) = 0 exactly (A = 0: pre-activation is exactly 0)."""
+    prob = _prob_nobias()
+    Z = torch.zeros_like(prob.A)
+    assert np.all(_run(prob, A=Z, act="sigmoid") == 0.5)
+    assert np.all(_run(prob, A=Z, act="tanh") == 0.0)
+
+
+def test_sigmoid_tanh_symmetries():
+    """sigma(-x) = 1 - sigma(x), tanh(-x) = -tanh(x): negating A negates pre exactly."""
+    prob = _prob_nobias()
+    for act, check in (("sigmoid", lambda a, b: np.abs(a + b - 1.0).max() < 1e-15),
+                       ("tanh", lambda a, b: np.abs(a + b).max() < 1e-15)):
+        assert check(_run(prob, act=act), _run(prob, A=-prob.A, act=act))
+
+
+def test_tanh_sigmoid_identity():
+    """tanh(x) = 2*sigma(2x) - 1 ties the two independent implementations; 2A is exact in fp16."""
+    prob = _prob_nobias()
+    t = _run(prob, act="tanh")
+    s2 = _run(prob, A=prob.A * 2, act="sigmoid")
+    assert np.abs(t - (2 * s2 - 1)).max() < 1e-14
+    assert 0.0 < s2.min() and s2.max() < 1.0
+
+
+def test_sigmoid_monotone_in_pre():
+    """The activation is applied to the same pre-activation: its order is preserved."""
+    prob = _prob_nobias(seed=61)
+    pre = _run(prob, act=None)
+    for act in ("sigmoid", "tanh"):
+        y = _run(prob, act=act)
+        o = np.argsort(pre.ravel(), kind="stable")
+        assert np.all(np.diff(y.ravel()[o]) >= 0)
+
+
+@pytest.mark.parametrize("act", [None, "relu", "sigmoid", "tanh"])
+def test_subtract_bias_is_add_of_negated_bias(act):
+    """A - bias == A + (-bias) bitwise (fp16 negation is exact) for every activation."""
+    prob = workloads.make_problem(37, 45, 53, seed=62, bias_mode="row")
+    a = _run(prob, act=act, bias=prob.bias, bias_sub=True)
+    b = _run(prob, act=act, bias=-prob.bias, bias_sub=False)
+    assert np.array_equal(a, b)
+    assert not np.array_equal(a, _run(prob, act=act, bias=prob.bias)) or act == "relu"
+
+
+# ---------------------------------------------------------------- sum of matmuls (Listing 4)
+def test_gemm2_golden_and_block_identity():
+    """Hand case: 1*2 + 3*4 - 4 = 10 (PAPER.md:1157-1166, S3 add then relu_add); and the block
+    identity A.B + P.Q = [A P].[B; Q] against the single-GEMM oracle on concatenated operands."""
+    one = lambda v: torch.tensor([[v]], dtype=torch.float16)
+    out, mag = oracle.gemm2_epilogue(one(1), one(2), one(3), one(4), 1, 1, 1, 1, bias=torch.tensor([-4.0]).half(),
+                                     bias_mode="row", act="relu")
+    assert out[0, 0] == 10.0 and mag[0, 0] == 14.0
+    M, N, K1, K2 = 40, 56, 48, 24
+    p1 = workloads.make_problem(M, N, K1, seed=70, bias_mode="col")
+    p2 = workloads.make_problem(M, N, K2, seed=71, bias_mode=None)
+    z, zm = oracle.gemm2_epilogue(p1.A, p1.B, p2.A, p2.B, M, N, K1, K2, bias=p1.bias, bias_mode="col", act="tanh")
+    cat = workloads.Problem(M, N, K1 + K2, torch.cat([p1.A, p2.A], 1), torch.cat([p1.B, p2.B], 0), p1.bias, None,
+                            {"bias_mode": "col", "prologue": None})
+    ref, rm = oracle_run(cat, "rr", act="tanh")
+    assert np.all(np.abs(z - ref) <= 1e-12 * (rm + 1))
+    assert np.allclose(zm, rm, rtol=1e-12)
+
+
+def test_gemm2_reductions():
+    """P = 0 reduces to the single GEMM (bitwise); swapping the two products commutes (bitwise)."""
+    M, N, K1, K2 = 33, 47, 40, 16
+    p1 = workloads.make_problem(M, N, K1, seed=72, bias_mode="row")
+    p2 = workloads.make_problem(M, N, K2, seed=73, bias_mode=None)
+    z0, _ = oracle.gemm2_epilogue(p1.A, p1.B, torch.zeros(M, K2, dtype=torch.float16), p2.B, M, N, K1, K2,
+                                  bias=p1.bias, act="relu")
+    single, _ = oracle_run(p1, "rr")
+    assert np.array_equal(z0, single)
+    pb = workloads.make_problem(M, N, K1, seed=74, bias_mode=None)
+    a, _ = oracle.gemm2_epilogue(p1.A, p1.B, pb.A, pb.B, M, N, K1, K1, bias=p1.bias, act=None)
+    b, _ = oracle.gemm2_epilogue(pb.A, pb.B, p1.A, p1.B, M, N, K1, K1, bias=p1.bias, act=None)
+    assert np.array_equal(a, b)
