@@ -338,8 +338,8 @@ def debug_stats(max_ctas: int = 148):
     n = load_library().ge_debug_read(buf.ctypes.data, max_ctas)
     keys = ("total", "prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0",
             "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math", "sk_owner_wait", "sk_partial_write",
-            "sk_pieces", "epi_end")
-    return [dict(zip(keys, (int(x) for x in buf[i, :14]))) for i in range(n)]
+            "sk_pieces", "epi_end", "reserved", "first_mma")
+    return [dict(zip(keys, (int(x) for x in buf[i, :16]))) for i in range(n)]
 
 
 def version() -> str:

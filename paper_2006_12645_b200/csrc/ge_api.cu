@@ -229,15 +229,19 @@ double config_eff(int bn, int cg) {
 // (K + exposed epilogue) / eff, waves = ceil(#tiles / #concurrent tiles).  Small problems pick
 // narrow tiles to fill the 148 SMs; large ones the CTA-pair tiles.
 Plan make_plan(const Args& a, int sms) {
-    constexpr double kExposedK = 192.0;      // accumulator drain of a single-buffered tile, in K units
-    // Partial write + flag handshake + read-back of a stream-K share, in K units: measured ~25K
-    // cycles on B200 (profiles/r01_stream_k.txt), i.e. about 50 k-blocks of a 256 x 256 pair tile.
-    constexpr double kStreamKCostK = 3200.0;
+    // Cost model in SM cycles, calibrated on B200:
+    //   one 64-deep k-block of a 128 x BN per-SM tile: 128*BN*64*2 / (8192 flop/clk * eff);
+    //   the single-buffered 256 x 512 tile exposes part of its accumulator drain per tile;
+    //   a stream-K launch adds its partial traffic (write + read-back of a 128 x BN fp32 slot per
+    //   CTA at ~16 B/clk, profiles/r01_stream_k.txt) plus a fixed handshake.
+    static const double sk_fixed = [] {
+        const char* e = getenv("GE_SK_FIXED_CYCLES");       // calibration override (tuning only)
+        return e ? atof(e) : 12000.0;
+    }();
     Plan best{};
     double best_cost = 0;
     const int cands[6][2] = {{512, 2}, {256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
-    const int64_t nkb = cdiv(a.K, 64) + cdiv(a.K2, 64);
-    const int64_t Ktot = a.K + a.K2;
+    const int64_t nkb = std::max<int64_t>(1, cdiv(a.K, 64) + cdiv(a.K2, 64));
     for (const auto& c : cands) {
         const int bn = c[0], cg = c[1];
         if (a.o.tile_n && a.o.tile_n != bn) continue;
@@ -248,21 +252,26 @@ Plan make_plan(const Args& a, int sms) {
         if (a.M <= 64 && !a.o.tile_n && !a.o.cta_group && !(bn == 128 && cg == 1)) continue;
         const int64_t tiles = a.batch * cdiv(a.M, 128 * cg) * cdiv(a.N, bn);
         const int64_t conc = std::max(1, sms / cg);
-        const double kk = static_cast<double>(std::max<int64_t>(Ktot, 64)) + (bn == 512 ? kExposedK : 0.0);
         double eff = config_eff(bn, cg);
         // The prologue transform rewrites each 16 KB A stage in smem: configurations with less MMA
         // time per stage than 256 x 512 pair tiles become shared-memory bound.
         if (a.o.prologue != GE_PRO_NONE && bn * cg < 1024) eff *= 0.55;
-        // data-parallel: whole waves of tiles
+        const double t_kb = 128.0 * bn * 64 * 2 / (8192.0 * eff);
+        const double drain = bn == 512 ? 3.0 * t_kb : 0.0;          // exposed per tile (single acc)
         const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
-        double cost = waves * (128.0 * bn) * kk / eff;
+        double cost = waves * (nkb * t_kb + drain);
         int64_t sk = 0;
-        // stream-K for the last partial wave (double-buffered accumulators only, DESIGN.md)
+        // stream-K for the last partial wave (double-buffered accumulators only)
         const int64_t rem = tiles % conc;
         const bool sk_ok = bn <= 256 && rem != 0 && nkb >= 2 && a.o.stream_k != 1;
         if (sk_ok) {
-            const double sk_waves = static_cast<double>(tiles / conc) + static_cast<double>(rem) / conc;
-            const double sk_cost = (sk_waves * kk + kStreamKCostK) * (128.0 * bn) / eff;
+            const double share = static_cast<double>(tiles / conc) * nkb + static_cast<double>(rem) * nkb / conc;
+            // measured: the owner reads one partial per contributor and every cluster's share ends at
+            // about the same time, so partial write + wait + read-back adds 10-25K cycles whatever the
+            // share (profiles/r01_stream_k.txt, r01_paper_sweep_stream_k.txt)
+            const int64_t contributors = std::max<int64_t>(1, conc / std::max<int64_t>(rem, 1));
+            const double partial = (1.0 + contributors) * 128.0 * bn * 4 / 16.0;
+            const double sk_cost = share * t_kb + partial + sk_fixed;
             if (a.o.stream_k == 2 || sk_cost < cost) {
                 cost = sk_cost;
                 sk = rem;

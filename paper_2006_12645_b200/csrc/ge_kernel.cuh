@@ -83,7 +83,7 @@ struct Params {
 enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
              DBG_EPI_REL0 = 5, DBG_EPI_REL1 = 6, DBG_EPI_TILE = 7, DBG_EPI_TMEMLD = 8,
              DBG_EPI_MATH = 9, DBG_SK_WAIT = 10, DBG_SK_WRITE = 11, DBG_SK_PIECES = 12, DBG_EPI_END = 13,
-             DBG_MMA_END = 14, DBG_SLOTS = 16 };
+             DBG_MMA_END = 14, DBG_FIRST_MMA = 15, DBG_SLOTS = 16 };
 
 template <int BN, int CG>
 struct Cfg {
@@ -199,8 +199,10 @@ __device__ __forceinline__ void activate(float* f, int n, int act) {
 #pragma unroll
         for (int e = 0; e < n; ++e) f[e] = f[e] > 0.0f ? f[e] : 0.0f;
     } else if (act == ACT_SIGMOID) {
+        // ex2.approx-based exp and a fast reciprocal: relative error ~1e-7, far below the fp16
+        // output rounding (2^-11) the bound allows; saturates to 0 / 1 at the extremes.
 #pragma unroll
-        for (int e = 0; e < n; ++e) f[e] = 1.0f / (1.0f + expf(-f[e]));
+        for (int e = 0; e < n; ++e) f[e] = __frcp_rn(1.0f + __expf(-f[e]));
     } else if (act == ACT_TANH) {
 #pragma unroll
         for (int e = 0; e < n; ++e) f[e] = tanhf(f[e]);
@@ -276,6 +278,11 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
+    // prefetch, cluster sync) overlapped the previous kernel's tail; wait for it to complete before
+    // touching global memory, then let the next launch in the stream get scheduled.
+    ptx::grid_dependency_wait();
+    ptx::launch_dependents();
 
     unsigned long long* dbg = p.dbg ? p.dbg + blockIdx.x * DBG_SLOTS : nullptr;
     const long long t_start = clock64();
@@ -364,6 +371,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
                 const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
                 const uint32_t d_tmem = tmem_base + acc * BN;
+                if (dbg && lane == 0 && it == 0) dbg[DBG_FIRST_MMA] = static_cast<unsigned long long>(clock64() - t_start);
                 // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
                 // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
                 // SBO = next 8-row K group (1024 B).

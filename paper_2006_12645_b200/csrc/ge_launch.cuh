@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "ge_kernel.cuh"
 
 namespace ge {
@@ -31,13 +33,21 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     cfg.blockDim = dim3(kernel_threads(OUT_F32, PRO), 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: the kernel's prologue may overlap the previous kernel's tail
+    // (the kernel waits on griddepcontrol.wait before touching global memory).  GE_PDL=0 disables.
+    static const bool pdl = [] {
+        const char* e = getenv("GE_PDL");
+        return !(e && e[0] == '0');
+    }();
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.c, m.p, m.q, p);
 }
 

@@ -28,3 +28,5 @@ print("  mma end (total) per leader: min", tots[0], "median", tots[len(tots)//2]
 print("  slowest CTAs (idx: epi_end, mma_end(total), owner_wait, partial_write, pieces, epi_tile):")
 for i, r in sorted(enumerate(st), key=lambda x: -x[1]["epi_end"])[:6]:
     print(f"    {i:3d}: {r['epi_end']:7d} {r['total']:7d} {r['sk_owner_wait']:7d} {r['sk_partial_write']:6d} {r['sk_pieces']} {r['epi_tile']:7d}")
+fm = sorted(r["first_mma"] for r in lead)
+print("  first MMA (cycles after kernel start) per leader: min", fm[0], "median", fm[len(fm)//2], "max", fm[-1])
