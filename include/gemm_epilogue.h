@@ -156,9 +156,10 @@ ge_status gemm2_epilogue(int64_t M, int64_t N, int64_t K1, int64_t K2,
 /*
  * Host-buffer variant (end-to-end path): same arguments as gemm_epilogue_batched but
  * A, B, bias, prologue_scale and C are HOST pointers (pinned memory gives full PCIe
- * bandwidth; pageable works).  The call copies the inputs to a library-owned device
- * workspace on `stream`, runs the fused kernel, copies C back and synchronizes `stream`
- * before returning.  The workspace grows on demand, is kept per device for reuse and is
+ * bandwidth and copy/compute overlap; pageable works).  The call copies B (and bias, scale) to
+ * a library-owned device workspace, then streams A and C in blocks (row blocks, or batch items)
+ * on library copy/compute streams so each block's kernel and C read-back overlap the next
+ * block's upload; it is ordered after prior work on `stream` and synchronizes before returning.  The workspace grows on demand, is kept per device for reuse and is
  * released by ge_release_workspace().  Operand alignment rules apply to ld/strides only.
  */
 ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K,

@@ -545,6 +545,33 @@ struct Workspace {
 std::mutex g_ws_mu;
 Workspace g_ws[64];
 
+// Copy/compute streams and events of the pipelined host-buffer path, one set per device
+// (used under g_ws_mu).
+constexpr int kPipeBlocks = 8;
+struct PipeStreams {
+    bool init = false, ok = false;
+    cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_in[kPipeBlocks] = {}, ev_out[kPipeBlocks] = {};
+};
+PipeStreams g_pipe[64];
+PipeStreams& pipe_streams(int dev) {
+    PipeStreams& p = g_pipe[dev & 63];
+    if (!p.init) {
+        p.init = true;
+        bool ok = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&p.cmp, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&p.ev_start, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&p.ev_end, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; ok && i < kPipeBlocks; ++i)
+            ok = cudaEventCreateWithFlags(&p.ev_in[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p.ev_out[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+        p.ok = ok;
+    }
+    return p;
+}
+
 }  // namespace
 
 namespace ge {
@@ -652,32 +679,94 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
     char* dBias = dB + up(nB);
     char* dS = dBias + up(nBias);
     char* dC = dS + up(nS);
-    cudaError_t e = cudaSuccess;
-    if (nA) e = cudaMemcpyAsync(dA, a.A, nA, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && nB) e = cudaMemcpyAsync(dB, a.B, nB, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && nBias) e = cudaMemcpyAsync(dBias, a.bias, nBias, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && nS) e = cudaMemcpyAsync(dS, a.o.prologue_scale, nS, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) {
+    // Pipelined end-to-end path: B, bias and scale go first, then A and C
+    // move in blocks (rows of A / C, or whole batch items) so that the GEMM and the C read-back of
+    // one block overlap the host->device copy of the next (separate copy engines per direction).
+    PipeStreams& ps = pipe_streams(dev);
+    if (!ps.ok) return fail(GE_ERR_CUDA, "could not create the copy/compute streams");
+    auto chk = [&](cudaError_t e, const char* what) {
+        if (e == cudaSuccess) return true;
         cudaGetLastError();
-        return fail(GE_ERR_CUDA, std::string("H2D copy failed: ") + cudaGetErrorString(e));
+        fail(GE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        return false;
+    };
+    if (!chk(cudaEventRecord(ps.ev_start, st), "event")) return GE_ERR_CUDA;
+    if (!chk(cudaStreamWaitEvent(ps.h2d, ps.ev_start, 0), "event")) return GE_ERR_CUDA;
+    if (nB && !chk(cudaMemcpyAsync(dB, a.B, nB, cudaMemcpyHostToDevice, ps.h2d), "H2D B")) return GE_ERR_CUDA;
+    if (nBias && !chk(cudaMemcpyAsync(dBias, a.bias, nBias, cudaMemcpyHostToDevice, ps.h2d), "H2D bias"))
+        return GE_ERR_CUDA;
+    if (nS && !chk(cudaMemcpyAsync(dS, a.o.prologue_scale, nS, cudaMemcpyHostToDevice, ps.h2d), "H2D scale"))
+        return GE_ERR_CUDA;
+    // blocks: batch items when batched, else row blocks (multiples of the 256-row pair tile)
+    const bool by_item = a.batch > 1;
+    const int64_t units = by_item ? a.batch : a.M;
+    int64_t nblk = by_item ? std::min<int64_t>(a.batch, kPipeBlocks) : std::min<int64_t>(kPipeBlocks, a.M / 1024);
+    nblk = std::max<int64_t>(nblk, 1);
+    int64_t per = cdiv(units, nblk);
+    if (!by_item) per = cdiv(per, 256) * 256;
+    nblk = cdiv(units, per);
+    for (int64_t blk = 0; blk < nblk; ++blk) {
+        const int64_t u0 = blk * per, u1 = std::min(units, u0 + per);
+        // host -> device: this block of A
+        if (nA) {
+            cudaError_t e;
+            if (by_item) {
+                const int64_t item = extent_bytes(1, arow ? a.M : a.K, arow ? a.K : a.M, a.lda, 0, 2);
+                const int64_t off = u0 * a.sA * 2, bytes = (u1 - u0 - 1) * a.sA * 2 + item;
+                e = cudaMemcpyAsync(dA + off, static_cast<const char*>(a.A) + off, bytes, cudaMemcpyHostToDevice,
+                                    ps.h2d);
+            } else if (arow) {
+                const int64_t off = u0 * a.lda * 2, bytes = ((u1 - u0 - 1) * a.lda + a.K) * 2;
+                e = cudaMemcpyAsync(dA + off, static_cast<const char*>(a.A) + off, bytes, cudaMemcpyHostToDevice,
+                                    ps.h2d);
+            } else {
+                e = cudaMemcpy2DAsync(dA + u0 * 2, a.lda * 2, static_cast<const char*>(a.A) + u0 * 2, a.lda * 2,
+                                      (u1 - u0) * 2, a.K, cudaMemcpyHostToDevice, ps.h2d);
+            }
+            if (!chk(e, "H2D A")) return GE_ERR_CUDA;
+        }
+        if (!chk(cudaEventRecord(ps.ev_in[blk], ps.h2d), "event")) return GE_ERR_CUDA;
+        if (!chk(cudaStreamWaitEvent(ps.cmp, ps.ev_in[blk], 0), "event")) return GE_ERR_CUDA;
+        // the fused kernel on this block
+        Args d = a;
+        d.B = nB ? dB : nullptr;
+        d.o.prologue_scale = nS ? reinterpret_cast<const float*>(dS) : nullptr;
+        if (by_item) {
+            d.batch = u1 - u0;
+            d.A = nA ? dA + u0 * a.sA * 2 : nullptr;
+            d.B = nB ? dB + u0 * a.sB * 2 : nullptr;
+            d.C = dC + u0 * a.sC * es;
+            d.bias = nBias ? dBias + u0 * a.sBias * 2 : nullptr;
+        } else {
+            d.M = u1 - u0;
+            d.A = nA ? dA + (arow ? u0 * a.lda : u0) * 2 : nullptr;
+            d.C = dC + u0 * a.ldc * es;
+            d.bias = nullptr;
+            if (nBias) {
+                const int64_t boff = a.o.bias_mode == GE_BIAS_ROW ? 0 : a.o.bias_mode == GE_BIAS_COL ? u0 : u0 * a.o.ldbias;
+                d.bias = dBias + boff * 2;
+            }
+        }
+        if (d.K > 0 && !d.A) d.A = dA;
+        s = launch(d, ps.cmp);
+        if (s != GE_OK) return s;
+        if (!chk(cudaEventRecord(ps.ev_out[blk], ps.cmp), "event")) return GE_ERR_CUDA;
+        if (!chk(cudaStreamWaitEvent(ps.d2h, ps.ev_out[blk], 0), "event")) return GE_ERR_CUDA;
+        // device -> host: the block's M x N window of C (the caller's padding is left untouched)
+        cudaError_t e = cudaSuccess;
+        if (by_item) {
+            for (int64_t b = u0; b < u1 && e == cudaSuccess; ++b)
+                e = cudaMemcpy2DAsync(static_cast<char*>(a.C) + b * a.sC * es, a.ldc * es, dC + b * a.sC * es,
+                                      a.ldc * es, a.N * es, a.M, cudaMemcpyDeviceToHost, ps.d2h);
+        } else {
+            e = cudaMemcpy2DAsync(static_cast<char*>(a.C) + u0 * a.ldc * es, a.ldc * es, dC + u0 * a.ldc * es,
+                                  a.ldc * es, a.N * es, u1 - u0, cudaMemcpyDeviceToHost, ps.d2h);
+        }
+        if (!chk(e, "D2H C")) return GE_ERR_CUDA;
     }
-    Args d = a;
-    d.A = nA ? dA : nullptr;
-    d.B = nB ? dB : nullptr;
-    d.bias = nBias ? dBias : nullptr;
-    d.o.prologue_scale = nS ? reinterpret_cast<const float*>(dS) : nullptr;
-    d.C = dC;
-    s = launch(d, st);
-    if (s != GE_OK) return s;
-    // copy back only the M x N elements of each item (the caller's padding is left untouched)
-    for (int64_t b = 0; b < a.batch && e == cudaSuccess; ++b)
-        e = cudaMemcpy2DAsync(static_cast<char*>(a.C) + b * a.sC * es, a.ldc * es, dC + b * a.sC * es, a.ldc * es,
-                              a.N * es, a.M, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(GE_ERR_CUDA, std::string("host path failed: ") + cudaGetErrorString(e));
-    }
+    if (!chk(cudaEventRecord(ps.ev_end, ps.d2h), "event")) return GE_ERR_CUDA;
+    if (!chk(cudaStreamWaitEvent(st, ps.ev_end, 0), "event")) return GE_ERR_CUDA;
+    if (!chk(cudaStreamSynchronize(st), "host path")) return GE_ERR_CUDA;
     return GE_OK;
 }
 

@@ -307,3 +307,37 @@ def test_gemm2_sum_of_matmuls(layouts, tile_n, cg):
             assert np.array_equal(got, exact_expect(out, torch.float16))
         else:
             check_bound(got, out, mag, "gemm2")
+
+
+@pytest.mark.parametrize("layouts,bias_mode", [("rr", "col"), ("cr", "full"), ("cc", "row")])
+def test_host_entry_pipelined_blocks(layouts, bias_mode):
+    """The pipelined host path (row blocks of A/C streamed on copy/compute streams) equals the
+    device path bitwise, for row- and column-major A and every bias mode; M spans 3 blocks."""
+    M, N, K = 2304 + 40, 264, 136
+    prob = workloads.make_problem(M, N, K, seed=47, bias_mode=bias_mode, ldbias=272 if bias_mode == "full" else None)
+    def host_view(logical, lay):
+        st, ld = workloads.store(logical, lay, (logical.shape[1 if lay == "r" else 0] + 7) // 8 * 8)
+        st = st.pin_memory()
+        R, Cc = logical.shape
+        return st[:, :Cc] if lay == "r" else st[:, :R].t()
+    Ah, Bh = host_view(prob.A, layouts[0]), host_view(prob.B, layouts[1])
+    bh = prob.bias.pin_memory()
+    kw = dict(bias_mode=bias_mode, tile_n=256, cta_group=2, stream_k=1)
+    Ch = ge.gemm_epilogue_host(Ah, Bh, bh, **kw)
+    A, B = dev_operands(prob, layouts)
+    Cd = ge.gemm_epilogue(A, B, prob.bias.cuda(), **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(Ch, Cd.cpu())
+
+
+def test_host_entry_batched_items():
+    batch, M, N, K = 5, 256, 192, 128
+    probs = [workloads.make_problem(M, N, K, seed=500 + b, bias_mode="row") for b in range(batch)]
+    A = torch.stack([p.A for p in probs]).pin_memory()
+    B = torch.stack([p.B for p in probs]).pin_memory()
+    bias = torch.stack([p.bias for p in probs]).pin_memory()
+    kw = dict(tile_n=128, cta_group=1, stream_k=1)     # same kernel configuration on both paths
+    Ch = ge.gemm_epilogue_host(A, B, bias, **kw)
+    Cd = ge.gemm_epilogue_batched(A.cuda(), B.cuda(), bias.cuda(), **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(Ch, Cd.cpu())
