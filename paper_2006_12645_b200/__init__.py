@@ -25,7 +25,10 @@ __all__ = ["gemm_epilogue", "gemm2_epilogue", "gemm_epilogue_batched", "gemm_epi
            "launch_count", "version", "library_path", "load_library", "layout_of", "Status"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libgemm_epilogue.so")
+# GE_DEBUG_STATS=1 selects the diagnostics build (python paper_2006_12645_b200/_build.py --debug-stats)
+# (GE_LIBRARY_FILE: dev A/B experiments with an alternative in-tree build of the same library)
+_LIB_PATH = os.environ.get("GE_LIBRARY_FILE") or os.path.join(
+    _PKG, "libgemm_epilogue_dbg.so" if os.environ.get("GE_DEBUG_STATS") else "libgemm_epilogue.so")
 _lib = None
 
 

@@ -30,6 +30,22 @@
 
 #include "ge_ptx.cuh"
 
+// Diagnostics counters (GE_DEBUG_STATS) exist only in the debug build (_build.py --debug-stats).
+#ifndef GE_DBG
+#define GE_DBG 0
+#endif
+// Stage release in pairs (one tcgen05.commit per two k-blocks) and an early readiness test of the
+// next stage; both trim the fixed per-k-block issue cost that bounds small-N tiles.
+#ifndef GE_PAIR_RELEASE
+#define GE_PAIR_RELEASE 1
+#endif
+#ifndef GE_EARLY_TEST
+#define GE_EARLY_TEST 0
+#endif
+#ifndef GE_EPI_ONE_WAITER
+#define GE_EPI_ONE_WAITER 1
+#endif
+
 namespace ge {
 
 constexpr int kBK = 64;                 // K per pipeline stage (64 fp16 = one 128-B swizzle row)
@@ -102,13 +118,14 @@ struct Cfg {
     static constexpr int kStagingBytes = kStagingBufs * kStagingSetBytes;
     static constexpr int kBiasBytes = BN * 2;                         // tile's ROW-bias slice (fp16)
     static constexpr int kStagesRaw = (kSmemBudget - 1024 - kStagingBytes - kBiasBytes - kBarBytes) / kStageBytes;
-    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : (GE_PAIR_RELEASE ? kStagesRaw & ~1 : kStagesRaw);
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStagingBytes + kBiasBytes + kBarBytes;
     // fp32 accumulator in TMEM: double-buffered when two fit in the 512 columns, else one buffer
     // drained half by half (per-half barriers let the next tile's first MMAs start early).
     static constexpr int kAccStages = 2 * BN <= 512 ? 2 : 1;
     static constexpr int kTmemCols = kAccStages * BN;
     static_assert(kStages >= 2, "not enough smem for a pipeline");
+    static_assert(!GE_PAIR_RELEASE || kStages % 2 == 0, "paired stage release needs an even ring");
     static_assert(kBarBytes >= (3 * 8 + 6) * 8 + 4, "barrier area");
     static_assert(kSmemBytes <= kSmemBudget, "smem overflow");
     static_assert(BN == 64 || BN == 128 || BN == 256 || (BN == 512 && CG == 2), "BN");
@@ -284,7 +301,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     ptx::grid_dependency_wait();
     ptx::launch_dependents();
 
-    unsigned long long* dbg = p.dbg ? p.dbg + blockIdx.x * DBG_SLOTS : nullptr;
+    // Diagnostics accumulate in registers (a global read-modify-write per barrier wait would add
+    // an L2 round trip to every pipeline step) and are flushed once per thread at teardown.
+    const bool dbg = GE_DBG && p.dbg != nullptr;
+    unsigned long long dl[DBG_SLOTS];
+#pragma unroll
+    for (int i = 0; i < DBG_SLOTS; ++i) dl[i] = 0;
     const long long t_start = clock64();
     const int cluster_id = blockIdx.x / CG;
     const int num_clusters = gridDim.x / CG;
@@ -306,7 +328,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const int m0 = mt * C_::kTileM + rank * kRowsPerCta;
                 const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
-                    ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg ? &dbg[DBG_PROD_EMPTY] : nullptr);
+                    // paired release: the MMA warp commits only the odd stage of each pair (that
+                    // commit covers the even stage's MMAs too), so wait once per pair on it
+                    if (!GE_PAIR_RELEASE) ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                    else if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
                     // sum of matmuls (Listing 4): k-blocks past A.B's come from P.Q, same accumulator
                     const bool second = kb >= p.num_k_blocks1;
                     const CUtensorMap* map_a = second ? &tmap_p : &tmap_a;
@@ -366,23 +391,33 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             const uint32_t b_base = ptx::smem_u32(smem_b);
             int s = 0, it = 0;
             uint32_t phase = 0;
+            bool next_ready = false;
             for (; it < work.count(); ++it) {
                 const Piece pc = work.get(it);
                 const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
                 const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                if (dbg && lane == 0 && it == 0) dbg[DBG_FIRST_MMA] = static_cast<unsigned long long>(clock64() - t_start);
+                if (dbg && lane == 0 && it == 0) dl[DBG_FIRST_MMA] = static_cast<unsigned long long>(clock64() - t_start);
                 // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
                 // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
-                // SBO = next 8-row K group (1024 B).
-                auto mma_one = [&](int stage, int kb, int h, int k) {
-                    const uint32_t sa = a_base + stage * C_::kAStage;
-                    const uint32_t sbh = b_base + stage * C_::kBStage + h * C_::kBBlockBytes;
-                    const uint64_t ad = A_MN ? ptx::make_sw128_desc(sa + k * 2048, 8192, 1024)
-                                             : ptx::make_sw128_desc(sa + k * 32, 0, 1024);
-                    const uint64_t bd = B_MN ? ptx::make_sw128_desc(sbh + k * 2048, 8192, 1024)
-                                             : ptx::make_sw128_desc(sbh + k * 32, 0, 1024);
-                    ptx::mma_f16_elect<CG>(d_tmem + h * C_::kUmmaN, ad, bd, IDESC, (kb != pc.kb0) || k != 0);
+                // SBO = next 8-row K group (1024 B).  Descriptors of a stage are the stage-0 ones
+                // plus the stage offset (the 14-bit address field cannot carry: smem < 256 KB).
+                const uint64_t a_desc0 = ptx::make_sw128_desc(a_base, A_MN ? 8192 : 0, 1024);
+                const uint64_t b_desc0 = ptx::make_sw128_desc(b_base, B_MN ? 8192 : 0, 1024);
+                constexpr int A_STEP = A_MN ? 2048 / 16 : 32 / 16;
+                constexpr int B_STEP = B_MN ? 2048 / 16 : 32 / 16;
+                auto desc_a = [&](int stage) {
+                    return a_desc0 + static_cast<uint64_t>((stage * C_::kAStage) >> 4);
+                };
+                auto desc_b = [&](int stage, int h) {
+                    return b_desc0 + static_cast<uint64_t>((stage * C_::kBStage + h * C_::kBBlockBytes) >> 4);
+                };
+                auto release_stage = [&](int stage) {
+                    if (!GE_PAIR_RELEASE || (stage & 1)) ptx::mma_commit_elect<CG>(&empty_bar[stage]);
+                };
+                auto mma_half = [&](int stage, int kb, int h) {
+                    ptx::mma_kblock<CG, A_STEP, B_STEP>(d_tmem + h * C_::kUmmaN, desc_a(stage), desc_b(stage, h), IDESC,
+                                                        kb != pc.kb0);
                 };
                 if constexpr (NH == 2) {
                     // Single 512-column accumulator, drained half by half by the epilogue.  Half-0
@@ -394,39 +429,34 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                         if (npend == S) {          // every stage is held: block until half 1 is drained
                             ptx::mbar_wait_timed(&tempty_bar[1], acc_phase ^ 1,
-                                                 (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                                                 dbg && lane == 0, dl[DBG_MMA_TEMPTY]);
                             h1_free = true;
                         }
                         if (h1_free && npend > 0) {
                             ptx::tc_fence_after();
                             for (int i = 0; i < npend; ++i) {
                                 const int st = (s_pend + i) % S;
-#pragma unroll
-                                for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(st, pc.kb0 + i, 1, k);
-                                ptx::mma_commit_elect<CG>(&empty_bar[st]);
+                                mma_half(st, pc.kb0 + i, 1);
+                                release_stage(st);
                             }
                             npend = 0;
                         }
-                        ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
+                        ptx::mbar_wait_timed(&ready[s], phase, dbg && lane == 0, dl[DBG_MMA_FULL]);
                         ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             ptx::mbar_wait_timed(&tempty_bar[0], acc_phase ^ 1,
-                                                 (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                                                 dbg && lane == 0, dl[DBG_MMA_TEMPTY]);
                             ptx::tc_fence_after();
                             h1_free = ptx::mbar_test(&tempty_bar[1], acc_phase ^ 1);
                             if (h1_free) ptx::tc_fence_after();
                             s_pend = s;
                         }
                         if (h1_free) {
-#pragma unroll
-                            for (int k = 0; k < kBK / kUmmaK; ++k) {
-                                mma_one(s, kb, 0, k);
-                                mma_one(s, kb, 1, k);
-                            }
-                            ptx::mma_commit_elect<CG>(&empty_bar[s]);
+                            ptx::mma_kblock2<CG, A_STEP, B_STEP>(d_tmem, desc_a(s), desc_b(s, 0), desc_b(s, 1), IDESC,
+                                                                 kb != pc.kb0);
+                            release_stage(s);
                         } else {
-#pragma unroll
-                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(s, kb, 0, k);
+                            mma_half(s, kb, 0);
                             ++npend;
                             h1_free = ptx::mbar_test(&tempty_bar[1], acc_phase ^ 1);
                         }
@@ -434,29 +464,34 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     }
                     if (npend > 0) {               // short tile: catch up before signalling the epilogue
                         ptx::mbar_wait_timed(&tempty_bar[1], acc_phase ^ 1,
-                                             (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                                             dbg && lane == 0, dl[DBG_MMA_TEMPTY]);
                         ptx::tc_fence_after();
                         for (int i = 0; i < npend; ++i) {
                             const int st = (s_pend + i) % S;
-#pragma unroll
-                            for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(st, pc.kb0 + i, 1, k);
-                            ptx::mma_commit_elect<CG>(&empty_bar[st]);
+                            mma_half(st, pc.kb0 + i, 1);
+                            release_stage(st);
                         }
                     }
                     ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
                 } else {
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
-                        ptx::mbar_wait_timed(&ready[s], phase, (dbg && lane == 0) ? &dbg[DBG_MMA_FULL] : nullptr);
+                        if (!(GE_EARLY_TEST && next_ready))
+                            ptx::mbar_wait_timed(&ready[s], phase, dbg && lane == 0, dl[DBG_MMA_FULL]);
                         ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             // first k-block of a tile: the epilogue must have drained this buffer
                             ptx::mbar_wait_timed(&tempty_bar[acc], acc_phase ^ 1,
-                                                 (dbg && lane == 0) ? &dbg[DBG_MMA_TEMPTY] : nullptr);
+                                                 dbg && lane == 0, dl[DBG_MMA_TEMPTY]);
                             ptx::tc_fence_after();
                         }
-#pragma unroll
-                        for (int k = 0; k < kBK / kUmmaK; ++k) mma_one(s, kb, 0, k);
-                        ptx::mma_commit_elect<CG>(&empty_bar[s]);    // smem slot free once these MMAs finish
+                        if (GE_EARLY_TEST) {
+                            // readiness of the next stage, tested before this stage's MMAs are issued
+                            // so the barrier round trip overlaps the issue
+                            const int sn = s + 1 == S ? 0 : s + 1;
+                            next_ready = ptx::mbar_test(&ready[sn], s + 1 == S ? phase ^ 1 : phase);
+                        }
+                        mma_half(s, kb, 0);
+                        release_stage(s);                         // smem slot free once these MMAs finish
                         if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
                         if (++s == S) { s = 0; phase ^= 1; }
                     }
@@ -510,7 +545,16 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 ptx::named_bar_sync(1, EPI_WARPS * 32);
             }
             if (nkb > 0) {
-                ptx::mbar_wait_timed(&tfull_bar[acc], acc_phase, (dbg && e_idx == 0 && lane == 0) ? &dbg[DBG_EPI_TFULL] : nullptr);
+                // One warp polls the accumulator barrier; the others sleep on a hardware named
+                // barrier (8 polling warps would contend with the MMA and TMA threads for the
+                // mbarrier unit during the whole mainloop).
+                if (GE_EPI_ONE_WAITER) {
+                    if (e_idx == 0)
+                        ptx::mbar_wait_timed(&tfull_bar[acc], acc_phase, dbg && lane == 0, dl[DBG_EPI_TFULL]);
+                    ptx::named_bar_sync(3, EPI_WARPS * 32);
+                } else {
+                    ptx::mbar_wait_timed(&tfull_bar[acc], acc_phase, dbg && e_idx == 0 && lane == 0, dl[DBG_EPI_TFULL]);
+                }
                 ptx::tc_fence_after();
             }
             const long long t_epi0 = (dbg && e_idx == 0) ? clock64() : 0;
@@ -529,7 +573,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             auto release = [&](const int h) {
                 if (nkb == 0) return;
                 if (dbg && e_idx == 0 && lane == 0)
-                    dbg[h == 0 ? DBG_EPI_REL0 : DBG_EPI_REL1] += static_cast<unsigned long long>(clock64() - t_epi0);
+                    dl[h == 0 ? DBG_EPI_REL0 : DBG_EPI_REL1] += static_cast<unsigned long long>(clock64() - t_epi0);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -652,7 +696,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             };
             int c_first = cluster_id;
             if constexpr (C_::kAccStages == 2) {
-                if (dbg && e_idx == 0 && lane == 0 && pc.kind != PIECE_FULL) dbg[DBG_SK_PIECES] += 1;
+                if (dbg && e_idx == 0 && lane == 0 && pc.kind != PIECE_FULL) dl[DBG_SK_PIECES] += 1;
                 if (pc.kind == PIECE_PARTIAL) {
                     const long long tw0 = clock64();
                     // partial accumulator -> this CTA's workspace slot (fp32, row = TMEM lane), then
@@ -675,7 +719,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     __threadfence();
                     ptx::named_bar_sync(2, EPI_WARPS * 32);
                     if (e_idx == 0 && lane == 0) ptx::st_release_gpu(p.sk_flags + cluster_id * CG + rank, 1u);
-                    if (dbg && e_idx == 0 && lane == 0) dbg[DBG_SK_WRITE] += static_cast<unsigned long long>(clock64() - tw0);
+                    if (dbg && e_idx == 0 && lane == 0) dl[DBG_SK_WRITE] += static_cast<unsigned long long>(clock64() - tw0);
                     continue;
                 }
                 if (pc.kind == PIECE_OWNER) {
@@ -686,7 +730,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         for (int c2 = c_first; c2 < cluster_id; ++c2)
                             if (work.has_units(c2)) ptx::spin_acquire_gpu(p.sk_flags + c2 * CG + rank, 1u);
                     ptx::named_bar_sync(2, EPI_WARPS * 32);
-                    if (dbg && e_idx == 0 && lane == 0) dbg[DBG_SK_WAIT] += static_cast<unsigned long long>(clock64() - tw0);
+                    if (dbg && e_idx == 0 && lane == 0) dl[DBG_SK_WAIT] += static_cast<unsigned long long>(clock64() - tw0);
                 }
             }
             // owner: add the published partials (ascending cluster order: deterministic)
@@ -729,8 +773,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (j == CPH - 1) release(h);
                         compute(h * CPH_ALL + j * NG + grp, v, packed[j]);
                         if (dbg && e_idx == 0 && lane == 0) {
-                            dbg[DBG_EPI_TMEMLD] += static_cast<unsigned long long>(tl1 - tl0);
-                            dbg[DBG_EPI_MATH] += static_cast<unsigned long long>(clock64() - tl1);
+                            dl[DBG_EPI_TMEMLD] += static_cast<unsigned long long>(tl1 - tl0);
+                            dl[DBG_EPI_MATH] += static_cast<unsigned long long>(clock64() - tl1);
                         }
                     }
 #pragma unroll
@@ -759,10 +803,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             if (work.has_units(c2)) ptx::st_relaxed_gpu(p.sk_flags + c2 * CG + rank, 0u);
                 }
             }
-            if (dbg && e_idx == 0 && lane == 0) dbg[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
+            if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
         }
         if (p.c_tma && lane == 0) ptx::bulk_wait<0>();
-        if (dbg && e_idx == 0 && lane == 0) dbg[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
+        if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
     } else if (PRO && warp >= 4 + EPI_WARPS) {
         // ===================== prologue transform of the A stage (in place, in smem) ==========
         const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
@@ -854,8 +898,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 
     // ---- teardown: every role done; the allocating warp frees TMEM
     __syncwarp();
-    if (dbg && warp == 1 && lane == 0) {
-        dbg[DBG_TOTAL] = static_cast<unsigned long long>(clock64() - t_start);
+    if (dbg) {
+        if (warp == 1 && lane == 0) dl[DBG_TOTAL] = static_cast<unsigned long long>(clock64() - t_start);
+        unsigned long long* dg = p.dbg + blockIdx.x * DBG_SLOTS;
+#pragma unroll
+        for (int i = 0; i < DBG_SLOTS; ++i)
+            if (dl[i]) atomicAdd(dg + i, dl[i]);
     }
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();

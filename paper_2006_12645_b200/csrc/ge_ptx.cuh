@@ -94,14 +94,14 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
 
 // Diagnostics variant: with acc != nullptr every wait is timed (try_wait with a suspend hint can
 // sleep inside its first call) and the cycles are added to *acc.
-__device__ __forceinline__ void mbar_wait_timed(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
-    if (!acc) {
+__device__ __forceinline__ void mbar_wait_timed(uint64_t* bar, uint32_t parity, bool on, unsigned long long& acc) {
+    if (!on) {
         mbar_wait(bar, parity);
         return;
     }
     const long long t0 = clock64();
     mbar_wait(bar, parity);
-    *acc += static_cast<unsigned long long>(clock64() - t0);
+    acc += static_cast<unsigned long long>(clock64() - t0);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -291,6 +291,63 @@ __device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a_desc, 
             "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
             ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+    }
+}
+
+// One k-block (K = 64) of MMAs from a single asm block: one elect.sync, the four K = 16 steps
+// addressed by adding the step (in 16-B descriptor units: 2 for K-major, 128 for MN-major) to the
+// stage's base descriptors, so no per-MMA descriptor math or uniform-register moves are needed
+// (per-MMA issue overhead is what bounds small-N tiles: scripts/probes/mma_rate.cu).  The first
+// MMA accumulates iff `accumulate`; the rest always do.  NH = 2 issues both 256-column halves
+// (B descriptors bd0 / bd1, accumulators d0 / d0 + 256) interleaved per K step.
+#define GE_MMA_KBLOCK_ASM(CGS)                                                                         \
+    "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                          \
+    "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"         \
+    "add.s64 a1, %1, %5;\n\tadd.s64 a2, a1, %5;\n\tadd.s64 a3, a2, %5;\n\t"                       \
+    "add.s64 b1, %2, %6;\n\tadd.s64 b2, b1, %6;\n\tadd.s64 b3, b2, %6;\n\t"                       \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], %1, %2, %3, p;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a1, b1, %3, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a2, b2, %3, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a3, b3, %3, t;\n\t}"
+
+template <int CG, int A_STEP, int B_STEP>
+__device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                           uint32_t accumulate) {
+    if constexpr (CG == 1) {
+        asm volatile(GE_MMA_KBLOCK_ASM("1")
+                     ::"r"(d_tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+    } else {
+        asm volatile(GE_MMA_KBLOCK_ASM("2")
+                     ::"r"(d_tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+    }
+}
+
+#define GE_MMA_KBLOCK2_ASM(CGS)                                                                        \
+    "{\n\t.reg .pred e, p, t;\n\t.reg .b32 d1;\n\t"                                               \
+    ".reg .b64 a1, a2, a3, b1, b2, b3, c1, c2, c3;\n\t"                                               \
+    "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, %5, %5;\n\t"         \
+    "add.u32 d1, %0, 256;\n\t"                                                                      \
+    "add.s64 a1, %1, %6;\n\tadd.s64 a2, a1, %6;\n\tadd.s64 a3, a2, %6;\n\t"                       \
+    "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"                       \
+    "add.s64 c1, %3, %7;\n\tadd.s64 c2, c1, %7;\n\tadd.s64 c3, c2, %7;\n\t"                       \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], %1, %2, %4, p;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [d1], %1, %3, %4, p;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a1, b1, %4, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [d1], a1, c1, %4, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a2, b2, %4, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [d1], a2, c2, %4, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a3, b3, %4, t;\n\t"                           \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [d1], a3, c3, %4, t;\n\t}"
+
+template <int CG, int A_STEP, int B_STEP>
+__device__ __forceinline__ void mma_kblock2(uint32_t d_tmem, uint64_t ad, uint64_t bd0, uint64_t bd1, uint32_t idesc,
+                                            uint32_t accumulate) {
+    if constexpr (CG == 1) {
+        asm volatile(GE_MMA_KBLOCK2_ASM("1")
+                     ::"r"(d_tmem), "l"(ad), "l"(bd0), "l"(bd1), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+    } else {
+        asm volatile(GE_MMA_KBLOCK2_ASM("2")
+                     ::"r"(d_tmem), "l"(ad), "l"(bd0), "l"(bd1), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
     }
 }
 

@@ -13,7 +13,7 @@ bias = torch.randn(N, device="cuda", dtype=torch.float16); C = torch.empty(M, N,
 for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk)
 torch.cuda.synchronize()
 st = ge.debug_stats()
-lead = [s for i, s in enumerate(st) if cg == 1 or i % 2 == 0]
+lead = [s for i, s in enumerate(st) if (cg == 1 or i % 2 == 0) and s["total"] > 0]   # active leaders
 def avg(k, rows): return sum(r[k] for r in rows) / max(1, len(rows))
 tot = avg("total", lead)
 print(f"{M}x{N}x{K} {lay} bn={bn} cg={cg}: total {tot:.0f} cyc/CTA(leader)")
