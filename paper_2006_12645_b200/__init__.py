@@ -132,7 +132,7 @@ def _workspace(device, stream_handle):
     """Zero-filled stream-K workspace for (device, stream), large enough for any plan (one fp32
     128 x 256 slot + one flag per SM).  Allocated through torch, so it is CUDA-graph safe; every
     launch leaves it zero-filled."""
-    key = (device.index, int(stream_handle))
+    key = (device.index if hasattr(device, "index") else int(device), int(stream_handle))
     ws = _workspaces.get(key)
     if ws is None:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
@@ -145,7 +145,16 @@ def clear_workspaces():
     _workspaces.clear()
 
 
+_opt_cache = {}
+
+
 def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, stream_k=0, ws=None):
+    """ge_options for these arguments; reused across calls with the same ones (per-call host cost)."""
+    key = (bias_mode, ldbias, prologue, scale.data_ptr() if scale is not None else 0, out_dtype, tile_n,
+           cta_group, stream_k, ws.data_ptr() if ws is not None else 0, ws.numel() if ws is not None else 0)
+    o = _opt_cache.get(key)
+    if o is not None:
+        return o
     o = GEOptions()
     o.stream_k = int(stream_k)
     o.workspace = ws.data_ptr() if ws is not None else None
@@ -157,12 +166,17 @@ def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, s
     o.out_dtype = 1 if out_dtype == torch.float32 else 0
     o.tile_n = int(tile_n)
     o.cta_group = int(cta_group)
+    if len(_opt_cache) > 512:
+        _opt_cache.clear()
+    _opt_cache[key] = o
     return o
 
 
-def _stream(stream) -> int:
+def _stream(stream, device_index: Optional[int] = None) -> int:
     if stream is None:
-        return torch.cuda.current_stream().cuda_stream
+        if device_index is None:
+            device_index = torch.cuda.current_device()
+        return torch._C._cuda_getCurrentRawStream(device_index)
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
@@ -210,7 +224,7 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     if out.stride(-1) != 1 and N > 1:
         raise ValueError("out must be row-major")
     ldbias, _ = _bias_ld(bias, bias_mode)
-    sh = _stream(stream)
+    sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
                  _workspace(A.device, sh) if stream_k != 1 else None)
     st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
@@ -242,7 +256,7 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
     if out is None:
         out = torch.empty((M, N), dtype=out_dtype, device=A.device)
     ldbias, _ = _bias_ld(bias, bias_mode)
-    sh = _stream(stream)
+    sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, None, None, out.dtype, tile_n, cta_group, stream_k,
                  _workspace(A.device, sh) if stream_k != 1 else None)
     st = lib.gemm2_epilogue(M, N, K1, K2, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb, P.data_ptr(), ldp,
@@ -276,7 +290,7 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
     batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A, B, bias, bias_mode, out)
     if out is None:
         out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
-    sh = _stream(stream)
+    sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
                  _workspace(A.device, sh) if stream_k != 1 else None)
     st = lib.gemm_epilogue_batched(batch, M, N, K, la, lb, A.data_ptr(), lda, sA, B.data_ptr(), ldb, sB,
