@@ -91,7 +91,8 @@ typedef struct {
     int32_t prologue;               /* ge_prologue_op */
     const float* prologue_scale;    /* SCALE_K only: device pointer (host pointer for *_host), length K */
     int32_t out_dtype;              /* ge_out_dtype */
-    int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128, 256; 512 with cta_group 2) */
+    int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128, 192, 256; 512 with
+                                       cta_group 2; 192 with cta_group 2 needs a column-major B) */
     int32_t cta_group;              /* 0 = heuristic; 1 = single-CTA tiles; 2 = CTA-pair tiles */
     int32_t stream_k;               /* 0 = heuristic; 1 = off; 2 = on whenever the last wave is partial */
     void* workspace;                /* optional device workspace for stream-K partials (see ge_plan's

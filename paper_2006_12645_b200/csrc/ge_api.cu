@@ -123,11 +123,13 @@ ge_status validate(Args& a) {
     if (o.bias_mode < GE_BIAS_ROW || o.bias_mode > GE_BIAS_FULL) return fail(GE_ERR_INVALID_VALUE, "bad bias_mode");
     if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_RELU) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
     if (o.out_dtype != GE_OUT_F16 && o.out_dtype != GE_OUT_F32) return fail(GE_ERR_INVALID_VALUE, "bad out_dtype");
-    if (o.tile_n != 0 && o.tile_n != 64 && o.tile_n != 128 && o.tile_n != 256 && o.tile_n != 512)
-        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 256 or 512");
+    if (o.tile_n != 0 && o.tile_n != 64 && o.tile_n != 128 && o.tile_n != 192 && o.tile_n != 256 && o.tile_n != 512)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 192, 256 or 512");
     if (o.cta_group < 0 || o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
     if (o.cta_group == 2 && o.tile_n == 64) return fail(GE_ERR_INVALID_VALUE, "cta_group 2 needs tile_n >= 128");
     if (o.cta_group == 1 && o.tile_n == 512) return fail(GE_ERR_INVALID_VALUE, "tile_n 512 needs cta_group 2");
+    if (o.cta_group == 2 && o.tile_n == 192 && a.lb == GE_ROW_MAJOR)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n 192 with cta_group 2 needs a column-major (K-major) B");
     if (o.stream_k < 0 || o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
     if (o.workspace_bytes < 0 || (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 15)))
         return fail(GE_ERR_INVALID_VALUE, "workspace must be 16-byte aligned with a non-negative size");
@@ -221,8 +223,8 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // pair tile moves the least operand data per flop (L2 and HBM) at the cost of a single,
 // non-double-buffered accumulator (its drain is partly exposed: kExposedK below).
 double config_eff(int bn, int cg) {
-    if (cg == 2) return bn == 512 ? 1.06 : bn == 256 ? 1.00 : 0.58;
-    return bn == 256 ? 0.92 : bn == 128 ? 0.52 : 0.30;
+    if (cg == 2) return bn == 512 ? 1.06 : bn == 256 ? 1.00 : bn == 192 ? 0.87 : 0.58;
+    return bn == 256 ? 0.92 : bn == 192 ? 0.82 : bn == 128 ? 0.52 : 0.30;
 }
 
 // Cost model: per-SM time ~ waves x per-SM tile area x
@@ -240,12 +242,13 @@ Plan make_plan(const Args& a, int sms) {
     }();
     Plan best{};
     double best_cost = 0;
-    const int cands[6][2] = {{512, 2}, {256, 2}, {256, 1}, {128, 2}, {128, 1}, {64, 1}};
+    const int cands[8][2] = {{512, 2}, {256, 2}, {192, 2}, {256, 1}, {192, 1}, {128, 2}, {128, 1}, {64, 1}};
     const int64_t nkb = std::max<int64_t>(1, cdiv(a.K, 64) + cdiv(a.K2, 64));
     for (const auto& c : cands) {
         const int bn = c[0], cg = c[1];
         if (a.o.tile_n && a.o.tile_n != bn) continue;
         if (a.o.cta_group && a.o.cta_group != cg) continue;
+        if (bn == 192 && cg == 2 && a.lb == GE_ROW_MAJOR) continue;     // pair tile needs a K-major B
         // Skinny M (<= 64 rows): most of every A stage is TMA zero-fill, the shape is HBM bound on B
         // and 128 x 128 tiles measure best (profiles/r01_tune_sweep.json); narrower tiles only add
         // A-stage traffic per useful byte.
@@ -514,9 +517,11 @@ ge_status launch(Args& a, cudaStream_t st) {
     if (pl.cg == 1) {
         if (pl.bn == 64) e = ge::launch_cg1_bn64(a_mn, b_mn, f32, pro, maps, p, grid, st);
         else if (pl.bn == 128) e = ge::launch_cg1_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else if (pl.bn == 192) e = ge::launch_cg1_bn192(a_mn, b_mn, f32, pro, maps, p, grid, st);
         else e = ge::launch_cg1_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
     } else {
         if (pl.bn == 128) e = ge::launch_cg2_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else if (pl.bn == 192) e = ge::launch_cg2_bn192(a_mn, b_mn, f32, pro, maps, p, grid, st);
         else if (pl.bn == 256) e = ge::launch_cg2_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
         else e = ge::launch_cg2_bn512(a_mn, b_mn, f32, pro, maps, p, grid, st);
     }
@@ -576,12 +581,18 @@ PipeStreams& pipe_streams(int dev) {
 
 namespace ge {
 int smem_bytes_for(int bn, int cg) {
-    if (cg == 1) return bn == 64 ? Cfg<64, 1>::kSmemBytes : bn == 128 ? Cfg<128, 1>::kSmemBytes : Cfg<256, 1>::kSmemBytes;
-    return bn == 128 ? Cfg<128, 2>::kSmemBytes : bn == 256 ? Cfg<256, 2>::kSmemBytes : Cfg<512, 2>::kSmemBytes;
+    if (cg == 1)
+        return bn == 64 ? Cfg<64, 1>::kSmemBytes : bn == 128 ? Cfg<128, 1>::kSmemBytes
+             : bn == 192 ? Cfg<192, 1>::kSmemBytes : Cfg<256, 1>::kSmemBytes;
+    return bn == 128 ? Cfg<128, 2>::kSmemBytes : bn == 192 ? Cfg<192, 2>::kSmemBytes
+         : bn == 256 ? Cfg<256, 2>::kSmemBytes : Cfg<512, 2>::kSmemBytes;
 }
 int stages_for(int bn, int cg) {
-    if (cg == 1) return bn == 64 ? Cfg<64, 1>::kStages : bn == 128 ? Cfg<128, 1>::kStages : Cfg<256, 1>::kStages;
-    return bn == 128 ? Cfg<128, 2>::kStages : bn == 256 ? Cfg<256, 2>::kStages : Cfg<512, 2>::kStages;
+    if (cg == 1)
+        return bn == 64 ? Cfg<64, 1>::kStages : bn == 128 ? Cfg<128, 1>::kStages
+             : bn == 192 ? Cfg<192, 1>::kStages : Cfg<256, 1>::kStages;
+    return bn == 128 ? Cfg<128, 2>::kStages : bn == 192 ? Cfg<192, 2>::kStages
+         : bn == 256 ? Cfg<256, 2>::kStages : Cfg<512, 2>::kStages;
 }
 }  // namespace ge
 
@@ -808,8 +819,9 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0,
                        GE_EPI_NONE, opt);
     if (batch < 0 || M < 0 || N < 0 || K < 0 || num_sms <= 0) return fail(GE_ERR_INVALID_VALUE, "bad plan arguments");
-    if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 256 && a.o.tile_n != 512)
-        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 256 or 512");
+    if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 192 && a.o.tile_n != 256 &&
+        a.o.tile_n != 512)
+        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 192, 256 or 512");
     if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
     if (a.o.stream_k < 0 || a.o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
     const Plan p = make_plan(a, num_sms);

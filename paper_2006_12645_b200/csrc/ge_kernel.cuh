@@ -123,12 +123,16 @@ struct Cfg {
     // fp32 accumulator in TMEM: double-buffered when two fit in the 512 columns, else one buffer
     // drained half by half (per-half barriers let the next tile's first MMAs start early).
     static constexpr int kAccStages = 2 * BN <= 512 ? 2 : 1;
-    static constexpr int kTmemCols = kAccStages * BN;
+    static constexpr int kTmemUsed = kAccStages * BN;
+    // tcgen05.alloc takes a power of two >= 32 columns
+    static constexpr int kTmemCols = kTmemUsed <= 32 ? 32 : kTmemUsed <= 64 ? 64 : kTmemUsed <= 128 ? 128
+                                   : kTmemUsed <= 256 ? 256 : 512;
     static_assert(kStages >= 2, "not enough smem for a pipeline");
     static_assert(!GE_PAIR_RELEASE || kStages % 2 == 0, "paired stage release needs an even ring");
     static_assert(kBarBytes >= (3 * 8 + 6) * 8 + 4, "barrier area");
     static_assert(kSmemBytes <= kSmemBudget, "smem overflow");
-    static_assert(BN == 64 || BN == 128 || BN == 256 || (BN == 512 && CG == 2), "BN");
+    static_assert(BN == 64 || BN == 128 || BN == 192 || BN == 256 || (BN == 512 && CG == 2), "BN");
+    static_assert(kTmemUsed <= 512, "TMEM");
 };
 
 __device__ __forceinline__ void decode_tile(const Params& p, long long t, int tile_m, int& b, int& mt, int& nt) {

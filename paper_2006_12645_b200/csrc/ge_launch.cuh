@@ -57,8 +57,12 @@ cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m
                          cudaStream_t st) {
     const int key = (a_mn ? 8 : 0) | (b_mn ? 4 : 0) | (f32 ? 2 : 0) | (pro ? 1 : 0);
     switch (key) {
-#define GE_CASE(K, AM, BM, F, P) \
-    case K: return launch_one<BN, AM, BM, F, P, CG>(m, p, grid, st);
+// (BN = 192 with CTA pairs stages 96 B rows per CTA: only K-major B, whose TMA box takes any row
+// count; an MN-major B stage is built from 64-column swizzle atoms.)
+#define GE_CASE(K, AM, BM, F, P)                                                  \
+    case K:                                                                       \
+        if constexpr (BM && BN == 192 && CG == 2) return cudaErrorInvalidValue;   \
+        else return launch_one<BN, AM, BM, F, P, CG>(m, p, grid, st);
         GE_CASE(0, false, false, false, false)
         GE_CASE(1, false, false, false, true)
         GE_CASE(2, false, false, true, false)
@@ -83,6 +87,8 @@ cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m
 // Defined in ge_inst_*.cu (one translation unit per configuration, compiled in parallel).
 cudaError_t launch_cg1_bn64(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg1_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn192(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn192(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg1_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);

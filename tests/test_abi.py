@@ -119,6 +119,9 @@ def test_validate_invalid_values(lib, ge):
     assert v(lib, opt=opts(ge, tile_n=96)) == S.INVALID_VALUE
     assert v(lib, opt=opts(ge, cta_group=3)) == S.INVALID_VALUE
     assert v(lib, opt=opts(ge, cta_group=2, tile_n=64)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, cta_group=1, tile_n=192)) == 0
+    assert v(lib, lb=1, opt=opts(ge, cta_group=2, tile_n=192)) == 0                # K-major B
+    assert v(lib, lb=0, opt=opts(ge, cta_group=2, tile_n=192)) == S.INVALID_VALUE  # pair 192 needs K-major B
     assert v(lib, opt=opts(ge, bias_mode=2, ldbias=64)) == S.INVALID_VALUE   # ldbias < N
     assert v(lib, batch=2, sC=100) == S.INVALID_VALUE   # output items would overlap
     assert v(lib, opt=opts(ge, stream_k=3)) == S.INVALID_VALUE
