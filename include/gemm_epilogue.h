@@ -94,7 +94,9 @@ typedef struct {
     int32_t tile_n;                 /* 0 = heuristic; else force the N tile (64, 128, 192, 256; 512 with
                                        cta_group 2; 192 with cta_group 2 needs a column-major B) */
     int32_t cta_group;              /* 0 = heuristic; 1 = single-CTA tiles; 2 = CTA-pair tiles */
-    int32_t stream_k;               /* 0 = heuristic; 1 = off; 2 = on whenever the last wave is partial */
+    int32_t stream_k;               /* 0 = heuristic (stream-K tail or split-K); 1 = off (data-parallel
+                                       tiles only); 2 = stream-K (never split-K) whenever the last
+                                       wave is partial */
     void* workspace;                /* optional device workspace for stream-K partials (see ge_plan's
                                        workspace_bytes); 16-byte aligned, ZERO-FILLED before its first
                                        use and left zero-filled by every launch; must not be shared by
@@ -197,13 +199,15 @@ const char* ge_last_error_detail(void);
  * Describes the configuration the heuristic picks for a shape (no device access): tile_m,
  * tile_n, cta_group, pipeline stages, the number of output tiles, how many of them run
  * stream-K (the last partial wave's tiles, whose K range is split evenly across all clusters;
- * partial sums are reduced in fixed order, so results stay run-to-run deterministic) and the
- * workspace bytes that needs.  Any output pointer may be NULL.
+ * partial sums are reduced in fixed order, so results stay run-to-run deterministic), the
+ * split-K factor (split_k > 1: every tile is computed by split_k clusters, one K-slice each, and
+ * the fp32 partials are reduce-scattered by column slice through the workspace in fixed order;
+ * only for few, long tiles) and the workspace bytes either needs.  Any output pointer may be NULL.
  */
 ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                   const ge_options* opt, int32_t num_sms,
                   int32_t* tile_m, int32_t* tile_n, int32_t* cta_group, int32_t* stages,
-                  int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes);
+                  int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes, int32_t* split_k);
 
 /* Number of fused kernels this library has launched in this process (for launch accounting). */
 uint64_t ge_launch_count(void);

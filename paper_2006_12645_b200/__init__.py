@@ -95,7 +95,7 @@ def load_library():
     lib.ge_plan.restype = I32
     lib.ge_plan.argtypes = [I64, I64, I64, I64, I32, I32, OPT, I32, ctypes.POINTER(I32), ctypes.POINTER(I32),
                             ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64),
-                            ctypes.POINTER(I64)]
+                            ctypes.POINTER(I64), ctypes.POINTER(I32)]
     lib.ge_launch_count.restype = ctypes.c_uint64
     lib.ge_launch_count.argtypes = []
     lib.ge_debug_read.restype = I32
@@ -129,14 +129,14 @@ _workspaces = {}
 
 
 def _workspace(device, stream_handle):
-    """Zero-filled stream-K workspace for (device, stream), large enough for any plan (one fp32
-    128 x 256 slot + one flag per SM).  Allocated through torch, so it is CUDA-graph safe; every
+    """Zero-filled stream-K / split-K workspace for (device, stream), large enough for any plan
+    (one fp32 128 x 256 slot, one flag and one tile counter per SM).  Allocated through torch, so it is CUDA-graph safe; every
     launch leaves it zero-filled."""
     key = (device.index if hasattr(device, "index") else int(device), int(stream_handle))
     ws = _workspaces.get(key)
     if ws is None:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
-        ws = torch.zeros(sms * (128 * 256 * 4 + 4), dtype=torch.uint8, device=device)
+        ws = torch.zeros(sms * (128 * 256 * 4 + 8), dtype=torch.uint8, device=device)
         _workspaces[key] = ws
     return ws
 
@@ -333,14 +333,14 @@ def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: i
          cta_group: int = 0, stream_k: int = 0, prologue: Optional[str] = None) -> dict:
     lib = load_library()
     o = _options("row", 0, prologue, None, torch.float16, tile_n, cta_group, stream_k)
-    tm, tn, cg, stg = (ctypes.c_int32() for _ in range(4))
+    tm, tn, cg, stg, spl = (ctypes.c_int32() for _ in range(5))
     nt, sk, wsb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
     st = lib.ge_plan(batch, M, N, K, 0 if layouts[0] == "r" else 1, 0 if layouts[1] == "r" else 1, ctypes.byref(o),
                      num_sms, ctypes.byref(tm), ctypes.byref(tn), ctypes.byref(cg), ctypes.byref(stg),
-                     ctypes.byref(nt), ctypes.byref(sk), ctypes.byref(wsb))
+                     ctypes.byref(nt), ctypes.byref(sk), ctypes.byref(wsb), ctypes.byref(spl))
     _check(st)
     return {"tile_m": tm.value, "tile_n": tn.value, "cta_group": cg.value, "stages": stg.value,
-            "num_tiles": nt.value, "stream_k_tiles": sk.value, "workspace_bytes": wsb.value}
+            "num_tiles": nt.value, "stream_k_tiles": sk.value, "workspace_bytes": wsb.value, "split_k": spl.value}
 
 
 def launch_count() -> int:

@@ -213,6 +213,7 @@ struct Plan {
     int64_t tiles;
     int64_t sk_tiles;      // tiles of the last, partial wave split stream-K across all clusters (0 = none)
     int64_t clusters;      // persistent clusters launched
+    int splits = 0;        // split-K: clusters per tile (0 = off; then clusters = tiles * splits)
 };
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -230,7 +231,36 @@ double config_eff(int bn, int cg) {
 // Cost model: per-SM time ~ waves x per-SM tile area x
 // (K + exposed epilogue) / eff, waves = ceil(#tiles / #concurrent tiles).  Small problems pick
 // narrow tiles to fill the 148 SMs; large ones the CTA-pair tiles.
-Plan make_plan(const Args& a, int sms) {
+// Co-resident split-K clusters per (BN index, S) on each device, queried once (0 = unknown: the
+// planner then uses its GPC estimate).
+struct SplitCap {
+    int cap[4][9];
+};
+std::mutex g_cap_mu;
+SplitCap g_cap[64];
+bool g_cap_done[64];
+const SplitCap* split_capacity() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g_cap_mu);
+    SplitCap& c = g_cap[dev & 63];
+    if (!g_cap_done[dev & 63]) {
+        const int bns[4] = {64, 128, 192, 256};
+        for (int i = 0; i < 4; ++i)
+            for (int S = 0; S <= 8; ++S) c.cap[i][S] = S >= 2 ? ge::clusters_cg1(bns[i], S) : 0;
+        g_cap_done[dev & 63] = true;
+        if (getenv("GE_PRINT_SPLIT_CAPACITY"))      // dev: calibration of the planner's fallback estimate
+            for (int i = 0; i < 4; ++i)
+                fprintf(stderr, "split capacity bn=%d: S=2..8: %d %d %d %d %d %d %d\n", bns[i], c.cap[i][2], c.cap[i][3],
+                        c.cap[i][4], c.cap[i][5], c.cap[i][6], c.cap[i][7], c.cap[i][8]);
+    }
+    return &c;
+}
+
+Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
     // Cost model in SM cycles, calibrated on B200:
     //   one 64-deep k-block of a 128 x BN per-SM tile: 128*BN*64*2 / (8192 flop/clk * eff);
     //   the single-buffered 256 x 512 tile exposes part of its accumulator drain per tile;
@@ -280,8 +310,39 @@ Plan make_plan(const Args& a, int sms) {
                 sk = rem;
             }
         }
+        int splits = 0;
+        // Split-K for few, long tiles, single-CTA tiles only: a cluster of S
+        // CTAs per tile, one K-slice each, partials reduce-scattered over distributed shared
+        // memory ((S-1)/S of a 128 x BN fp32 tile sent per CTA at ~32 B/clk, plus the handshake).
+        // Co-resident clusters of S come from cudaOccupancyMaxActiveClusters (GPC-bound).
+        if (cg == 1 && bn <= 256 && a.o.stream_k == 0 && nkb >= 8) {
+            const int64_t smax = std::min<int64_t>(8, nkb / 4);
+            for (int64_t S = 2; S <= smax; ++S) {
+                const int64_t units = 4 * bn / 32;
+                const int64_t recv = cdiv(units, S) * (S - 1) * 32 * 32 * 4;
+                if (recv > static_cast<int64_t>(ge::stages_for(bn, 1)) * (128 + bn) * 64 * 2) continue;
+                const int bi = bn == 64 ? 0 : bn == 128 ? 1 : bn == 192 ? 2 : 3;
+                // fallback (no device): cudaOccupancyMaxActiveClusters measured on B200, S = 2..8
+                static const int kCap148[9] = {0, 0, 74, 45, 33, 26, 22, 15, 15};
+                int64_t conc_s = (cap && cap->cap[bi][S] > 0) ? cap->cap[bi][S]
+                                                              : static_cast<int64_t>(kCap148[S] * (sms / 148.0));
+                conc_s = std::max<int64_t>(1, conc_s);
+                const double red = (S - 1.0) / S * 128.0 * bn * 4 / 32.0 + 2500.0;
+                const double c_split = static_cast<double>(cdiv(tiles, conc_s)) *
+                                       (static_cast<double>(cdiv(nkb, S)) * t_kb + red);
+                if (c_split < cost * (1 - 1e-9)) {
+                    cost = c_split;
+                    splits = static_cast<int>(S);
+                    sk = 0;
+                }
+            }
+        }
         if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
             best = Plan{bn, cg, ge::stages_for(bn, cg), tiles, sk, sk ? conc : std::min<int64_t>(tiles, conc)};
+            if (splits) {
+                best.splits = splits;
+                best.clusters = tiles * splits;
+            }
             best_cost = cost;
         }
     }
@@ -294,7 +355,7 @@ Plan make_plan(const Args& a, int sms) {
 size_t sk_workspace_bytes(const Plan& pl) {
     if (!pl.sk_tiles) return 0;
     const size_t ctas = static_cast<size_t>(pl.clusters * pl.cg);
-    return ctas * 128 * pl.bn * 4 + ctas * 4;
+    return pl.splits ? 0 : ctas * 128 * pl.bn * 4 + ctas * 4;       // split-K reduces in DSMEM
 }
 
 struct SkWorkspace {
@@ -405,7 +466,7 @@ ge_status launch(Args& a, cudaStream_t st) {
     int sms = 0;
     s = device_info(&sms);
     if (s != GE_OK) return s;
-    const Plan pl = make_plan(a, sms);
+    const Plan pl = make_plan(a, sms, split_capacity());
     const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
     const bool a_mn = !arow, b_mn = brow;          // row-major A is K-major; row-major B is N(MN)-major
     const bool f32 = a.o.out_dtype == GE_OUT_F32;
@@ -494,6 +555,7 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.sk_units = 0;
     p.sk_ws = nullptr;
     p.sk_flags = nullptr;
+    p.splits = plan.splits;
     if (plan.sk_tiles) {
         const size_t need = sk_workspace_bytes(plan);
         void* ws = nullptr;
@@ -580,6 +642,10 @@ PipeStreams& pipe_streams(int dev) {
 }  // namespace
 
 namespace ge {
+int clusters_cg1(int bn, int cluster) {
+    return bn == 64 ? clusters_cg1_bn64(cluster) : bn == 128 ? clusters_cg1_bn128(cluster)
+         : bn == 192 ? clusters_cg1_bn192(cluster) : clusters_cg1_bn256(cluster);
+}
 int smem_bytes_for(int bn, int cg) {
     if (cg == 1)
         return bn == 64 ? Cfg<64, 1>::kSmemBytes : bn == 128 ? Cfg<128, 1>::kSmemBytes
@@ -814,7 +880,8 @@ const char* ge_last_error_detail(void) { return g_detail.c_str(); }
 
 ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                   const ge_options* opt, int32_t num_sms, int32_t* tile_m, int32_t* tile_n, int32_t* cta_group,
-                  int32_t* stages, int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes) {
+                  int32_t* stages, int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes,
+                  int32_t* split_k) {
     g_detail.clear();
     Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0,
                        GE_EPI_NONE, opt);
@@ -824,7 +891,7 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
         return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 192, 256 or 512");
     if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
     if (a.o.stream_k < 0 || a.o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
-    const Plan p = make_plan(a, num_sms);
+    const Plan p = make_plan(a, num_sms, split_capacity());     // (nullptr without a device)
     if (tile_m) *tile_m = 128 * p.cg;
     if (tile_n) *tile_n = p.bn;
     if (cta_group) *cta_group = p.cg;
@@ -832,6 +899,7 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     if (num_tiles) *num_tiles = p.tiles;
     if (stream_k_tiles) *stream_k_tiles = p.sk_tiles;
     if (workspace_bytes) *workspace_bytes = static_cast<int64_t>(sk_workspace_bytes(p));
+    if (split_k) *split_k = p.splits > 1 ? p.splits : 1;
     return GE_OK;
 }
 

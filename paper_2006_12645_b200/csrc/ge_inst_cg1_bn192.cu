@@ -6,4 +6,5 @@ cudaError_t launch_cg1_bn192(bool a_mn, bool b_mn, bool f32, bool pro, const Map
                             cudaStream_t st) {
     return launch_bn_cg<192, 1>(a_mn, b_mn, f32, pro, m, p, grid, st);
 }
+int clusters_cg1_bn192(int cluster) { return max_active_clusters<192, 1>(cluster); }
 }  // namespace ge

@@ -6,4 +6,5 @@ cudaError_t launch_cg1_bn256(bool a_mn, bool b_mn, bool f32, bool pro, const Map
                             cudaStream_t st) {
     return launch_bn_cg<256, 1>(a_mn, b_mn, f32, pro, m, p, grid, st);
 }
+int clusters_cg1_bn256(int cluster) { return max_active_clusters<256, 1>(cluster); }
 }  // namespace ge

@@ -89,6 +89,10 @@ struct Params {
     long long dp_tiles, sk_units;
     float* sk_ws;
     unsigned int* sk_flags;
+    // split-K: splits > 1 (single-CTA tiles only) launches clusters of
+    // `splits` CTAs per tile, CTA rank = K-slice; the fp32 partials are reduce-scattered through
+    // distributed shared memory inside the cluster
+    int splits;
     // diagnostics (GE_DEBUG_STATS): per-CTA blocked-cycle counters, or nullptr
     unsigned long long* dbg;
     int dbg_noload;                 // dev experiment only: stop issuing TMA after the ring is full once
@@ -112,7 +116,7 @@ struct Cfg {
     static constexpr int kAStage = kRowsPerCta * kBK * 2;             // 16 KB
     static constexpr int kBStage = kBRows * kBK * 2;
     static constexpr int kStageBytes = kAStage + kBStage;
-    static constexpr int kBarBytes = 256;                             // (3S + 6) mbarriers + TMEM slot
+    static constexpr int kBarBytes = 320;                             // (3S + 8) mbarriers + TMEM slot
     // Epilogue staging buffers per warp (double-buffered TMA stores).
     static constexpr int kStagingBufs = 2;
     static constexpr int kStagingBytes = kStagingBufs * kStagingSetBytes;
@@ -129,7 +133,7 @@ struct Cfg {
                                    : kTmemUsed <= 256 ? 256 : 512;
     static_assert(kStages >= 2, "not enough smem for a pipeline");
     static_assert(!GE_PAIR_RELEASE || kStages % 2 == 0, "paired stage release needs an even ring");
-    static_assert(kBarBytes >= (3 * 8 + 6) * 8 + 4, "barrier area");
+    static_assert(kBarBytes >= (3 * 8 + 8) * 8 + 4, "barrier area");
     static_assert(kSmemBytes <= kSmemBudget, "smem overflow");
     static_assert(BN == 64 || BN == 128 || BN == 192 || BN == 256 || (BN == 512 && CG == 2), "BN");
     static_assert(kTmemUsed <= 512, "TMEM");
@@ -153,7 +157,7 @@ __device__ __forceinline__ void decode_tile(const Params& p, long long t, int ti
 // t = cid, cid + G, ... < dp_tiles, then the cluster's share [u0, u1) of the stream-K units
 // (k-blocks of tiles dp_tiles .. num_tiles-1, tile-major), cut at tile boundaries.  The host keeps
 // the stream-K tiles fewer than the clusters, so a share spans at most two pieces.
-enum : int { PIECE_FULL = 0, PIECE_OWNER = 1, PIECE_PARTIAL = 2 };
+enum : int { PIECE_FULL = 0, PIECE_OWNER = 1, PIECE_PARTIAL = 2, PIECE_SPLIT = 3 };
 struct Piece {
     long long tile;
     int kb0, kb1;                   // k-block range [kb0, kb1) of the tile
@@ -162,11 +166,18 @@ struct Piece {
 
 struct WorkSeq {
     long long dp_tiles, units, u0, u1;
-    int cid, G, nkb, n_dp, n_sk;
+    int cid, G, nkb, n_dp, n_sk, splits;
     __device__ __forceinline__ WorkSeq(const Params& p, int cid_, int G_) {
         cid = cid_;
         G = G_;
         nkb = p.num_k_blocks;
+        splits = p.splits;
+        if (splits > 1) {                   // split-K: one K-slice of one tile per cluster
+            dp_tiles = units = u0 = u1 = 0;
+            n_dp = 0;
+            n_sk = (cid < p.num_tiles * splits) ? 1 : 0;
+            return;
+        }
         dp_tiles = p.dp_tiles;
         units = p.sk_units;
         n_dp = dp_tiles > cid ? static_cast<int>((dp_tiles - cid + G - 1) / G) : 0;
@@ -179,6 +190,14 @@ struct WorkSeq {
     __device__ __forceinline__ int count() const { return n_dp + n_sk; }
     __device__ __forceinline__ Piece get(int i) const {
         Piece pc;
+        if (splits > 1) {
+            const int j = cid % splits;
+            pc.tile = cid / splits;
+            pc.kb0 = j * nkb / splits;
+            pc.kb1 = (j + 1) * nkb / splits;
+            pc.kind = PIECE_SPLIT;
+            return pc;
+        }
         if (i < n_dp) {
             pc.tile = cid + static_cast<long long>(i) * G;
             pc.kb0 = 0;
@@ -266,7 +285,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     uint64_t* xform_bar = bars + 2 * S;         // [S] transform -> MMA (PRO only)
     uint64_t* tfull_bar = bars + 3 * S;         // [acc] MMA -> epilogue
     uint64_t* tempty_bar = bars + 3 * S + 2;    // [acc * NH + half] epilogue -> MMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 6);
+    uint64_t* peer_ready_bar = bars + 3 * S + 6;  // split-K: every peer's ring is free to receive
+    uint64_t* recv_full_bar = bars + 3 * S + 7;   // split-K: all partials addressed to this CTA landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 8);
+    const bool split_cluster = (CG == 1) && p.splits > 1;
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -292,11 +314,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         }
         for (int b = 0; b < 2; ++b) ptx::mbar_init(&tfull_bar[b], 1);
         for (int b = 0; b < 4; ++b) ptx::mbar_init(&tempty_bar[b], EPI_WARPS * CG);
+        ptx::mbar_init(peer_ready_bar, split_cluster ? p.splits - 1 : 1);
+        ptx::mbar_init(recv_full_bar, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
     ptx::tc_fence_before();
-    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
@@ -700,6 +724,75 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             };
             int c_first = cluster_id;
             if constexpr (C_::kAccStages == 2) {
+                if (pc.kind == PIECE_SPLIT) {
+                    // Split-K reduce-scatter over distributed shared memory.
+                    // The cluster's S CTAs hold the S K-slices of one tile.  Its output is cut into
+                    // U = 4 x NCHUNK units (TMEM lane quarter q x 32-column chunk c, u = 4c + q) and
+                    // split js owns units [u_lo(js), u_lo(js + 1)).  Every CTA st.async-es its fp32
+                    // partial of each unit it does not own into the owner's (now idle) pipeline
+                    // ring; the owner adds the S - 1 received partials to its own in ascending
+                    // split order (deterministic) and runs the usual bias / activation / store.
+                    const int S = p.splits;
+                    const int js = cluster_id % S;                     // == %cluster_ctarank
+                    constexpr int U = 4 * NCHUNK;
+                    constexpr int UB = 32 * W * 4;                     // bytes of one unit (32 rows x 32 fp32)
+                    auto owner = [&](int c) { return (4 * c + q) * S / U; };
+                    auto u_lo = [&](int o) { return (o * U + S - 1) / S; };
+                    const uint32_t recv_base = ptx::smem_u32(smem_a);
+                    if (e_idx == 0 && lane == 0) {
+                        // incoming bytes of this CTA's units; then tell every peer its ring is free
+                        ptx::mbar_arrive_expect_tx(recv_full_bar, static_cast<uint32_t>((u_lo(js + 1) - u_lo(js)) * (S - 1) * UB));
+                        for (int jj = 0; jj < S; ++jj)
+                            if (jj != js) ptx::mbar_arrive_cluster(peer_ready_bar, static_cast<uint32_t>(jj));
+                    }
+                    const long long tw0 = clock64();
+                    ptx::mbar_wait(peer_ready_bar, 0);
+                    if (dbg && e_idx == 0 && lane == 0) dl[DBG_SK_WAIT] += static_cast<unsigned long long>(clock64() - tw0);
+#pragma unroll 1
+                    for (int j = 0; j < CPH; ++j) {
+                        const int c = j * NG + grp;
+                        const int o = owner(c);
+                        if (o == js) continue;
+                        uint32_t v[W];
+                        load(c, v);
+                        ptx::tmem_ld_wait();
+                        const int slot = (4 * c + q - u_lo(o)) * (S - 1) + (js < o ? js : js - 1);
+                        const uint32_t dst = ptx::mapa_shared(recv_base + slot * UB + lane * 16, static_cast<uint32_t>(o));
+                        const uint32_t rbar = ptx::mapa_shared(ptx::smem_u32(recv_full_bar), static_cast<uint32_t>(o));
+#pragma unroll
+                        for (int g = 0; g < W / 4; ++g)
+                            ptx::st_async_v4(dst + g * 512, v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3], rbar);
+                    }
+                    const long long tr0 = clock64();
+                    ptx::mbar_wait(recv_full_bar, 0);
+                    if (dbg && e_idx == 0 && lane == 0) dl[DBG_SK_WRITE] += static_cast<unsigned long long>(clock64() - tr0);
+#pragma unroll 1
+                    for (int j = 0; j < CPH; ++j) {
+                        const int c = j * NG + grp;
+                        if (owner(c) != js) continue;
+                        uint32_t v[W];
+                        load(c, v);
+                        ptx::tmem_ld_wait();
+                        const uint8_t* rb = smem_a + (4 * c + q - u_lo(js)) * (S - 1) * UB + lane * 16;
+#pragma unroll 1
+                        for (int s2 = 0; s2 < S - 1; ++s2) {
+#pragma unroll
+                            for (int g = 0; g < W / 4; ++g) {
+                                const float4 pv = *reinterpret_cast<const float4*>(rb + s2 * UB + g * 512);
+                                v[4 * g] = __float_as_uint(__uint_as_float(v[4 * g]) + pv.x);
+                                v[4 * g + 1] = __float_as_uint(__uint_as_float(v[4 * g + 1]) + pv.y);
+                                v[4 * g + 2] = __float_as_uint(__uint_as_float(v[4 * g + 2]) + pv.z);
+                                v[4 * g + 3] = __float_as_uint(__uint_as_float(v[4 * g + 3]) + pv.w);
+                            }
+                        }
+                        uint32_t w[NWORD];
+                        compute(c, v, w);
+                        store(c, w);
+                    }
+                    release(0);
+                    if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
+                    continue;
+                }
                 if (dbg && e_idx == 0 && lane == 0 && pc.kind != PIECE_FULL) dl[DBG_SK_PIECES] += 1;
                 if (pc.kind == PIECE_PARTIAL) {
                     const long long tw0 = clock64();
@@ -910,7 +1003,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             if (dl[i]) atomicAdd(dg + i, dl[i]);
     }
     ptx::tc_fence_before();
-    if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+    if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<CG>(tmem_base, C_::kTmemCols);

@@ -35,7 +35,8 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    // CTA pairs; or, for split-K single-CTA tiles, one cluster per tile of `splits` CTAs (K-slices)
+    attr[0].val.clusterDim.x = (CG == 1 && p.splits > 1) ? p.splits : CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     // programmatic dependent launch: the kernel's prologue may overlap the previous kernel's tail
@@ -49,6 +50,35 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, m.a, m.b, m.c, m.p, m.q, p);
+}
+
+// Co-resident clusters of `cluster` CTAs of the (BN, CG) kernel on the current device (0 if the
+// query fails); the split-K planner uses it (cluster scheduling is GPC-bound, not SM-count-bound).
+template <int BN, int CG>
+int max_active_clusters(int cluster) {
+    auto kern = ge_fused_kernel<BN, false, false, false, false, CG>;
+    constexpr int smem = Cfg<BN, CG>::kSmemBytes;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cluster * 64, 1, 1);
+    cfg.blockDim = dim3(kernel_threads(false, false), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cluster;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
 // Dispatch over the 16 (A_MN, B_MN, OUT_F32, PRO) variants of one (BN, CG) configuration.
@@ -89,6 +119,11 @@ cudaError_t launch_cg1_bn64(bool, bool, bool, bool, const Maps&, const Params&, 
 cudaError_t launch_cg1_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg1_bn192(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn192(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+int clusters_cg1(int bn, int cluster);     // max_active_clusters of the single-CTA kernels (ge_inst_cg1_*.cu)
+int clusters_cg1_bn64(int cluster);
+int clusters_cg1_bn128(int cluster);
+int clusters_cg1_bn192(int cluster);
+int clusters_cg1_bn256(int cluster);
 cudaError_t launch_cg1_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);

@@ -121,6 +121,22 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
         : "memory");
 }
 
+// Shared::cluster address of the same smem offset in CTA `cta` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(cta));
+    return r;
+}
+
+// Asynchronous 16-B store into another CTA's shared memory (distributed shared memory); the bytes
+// are credited to that CTA's mbarrier (complete_tx), so no fence or flag is needed.
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(remote_addr), "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -140,7 +156,8 @@ __device__ __forceinline__ void spin_acquire_gpu(const unsigned int* p, unsigned
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
         if (v == want) return;
         if (clock64() - t0 > (1ll << 36)) asm volatile("trap;");
-        __nanosleep(64);
+        // no __nanosleep back-off: its wake-up granularity (microseconds) delayed every handoff;
+        // the acquire load's own L2 round trip paces the loop
     }
 }
 

@@ -168,6 +168,13 @@ def test_plan_tiles(ge):
     assert p["workspace_bytes"] == 148 * (128 * 256 * 4 + 4)
     assert ge.plan(4096, 4096, 4096, tile_n=256, cta_group=2, stream_k=1)["stream_k_tiles"] == 0
     assert ge.plan(8192, 8192, 8192, tile_n=512, cta_group=2, stream_k=2)["stream_k_tiles"] == 0   # 1-buffer acc
+    # split-K: few long tiles -> clusters of S single-CTA tiles reducing in DSMEM (no workspace)
+    p = ge.plan(2048, 128, 3456, layouts="rc")
+    assert p["cta_group"] == 1 and 2 <= p["split_k"] <= 8 and p["workspace_bytes"] == 0
+    assert p["num_tiles"] * p["split_k"] <= 148
+    assert ge.plan(2048, 128, 3456, layouts="rc", stream_k=1)["split_k"] == 1               # off
+    assert ge.plan(8192, 8192, 8192)["split_k"] == 1
+    assert ge.plan(2048, 128, 3456, layouts="rc", cta_group=2)["split_k"] == 1             # pairs never split
     with pytest.raises(ge.GEError):
         ge.plan(8192, 8192, 8192, tile_n=96)
 

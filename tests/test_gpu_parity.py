@@ -263,6 +263,99 @@ def test_stream_k_library_workspace_via_host_entry():
     assert np.array_equal(Ch.float().numpy().astype(np.float64), exact_expect(out, torch.float16))
 
 
+# ------------------------------------------------------------------ split-K (few, long tiles)
+SPLIT_SHAPES = [(640, 1024, 3840), (2048, 128, 3456), (128, 2176, 3200), (384, 768, 1536), (300, 520, 2000)]
+
+
+@pytest.mark.parametrize("M,N,K", SPLIT_SHAPES)
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_split_k_exact_and_bound(M, N, K, layouts):
+    """Split-K reduce-scatter: bias and activation applied once, after the full
+    reduction (R-C13); bitwise exact on small integers, within the bound on uniform data."""
+    p = ge.plan(M, N, K, layouts=layouts)
+    assert p["split_k"] > 1, p
+    for kind in ("smallint", "uniform"):
+        prob = workloads.make_problem(M, N, K, seed=45, kind=kind, bias_mode="row")
+        got = run_gpu(prob, layouts)
+        out, mag = oracle_run(prob, layouts)
+        if kind == "smallint":
+            assert np.array_equal(got, exact_expect(out, torch.float16))
+        else:
+            check_bound(got, out, mag, f"split-K {M}x{N}x{K} {layouts}")
+
+
+def test_split_k_deterministic_and_graph():
+    """Fixed-order DSMEM reduction: bitwise reproducible across launches and CUDA-graph replays,
+    equal to the data-parallel result within the bound."""
+    M, N, K = 640, 1024, 3840
+    assert ge.plan(M, N, K, layouts="rc")["split_k"] > 1
+    prob = workloads.make_problem(M, N, K, seed=46, bias_mode="row")
+    A, B = dev_operands(prob, "rc")
+    bias = prob.bias.cuda()
+    c1 = ge.gemm_epilogue(A, B, bias)
+    c2 = ge.gemm_epilogue(A, B, bias)
+    out = torch.empty_like(c1)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ge.gemm_epilogue(A, B, bias, out=out)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, c1)
+    assert torch.equal(c1, c2)
+    dp = ge.gemm_epilogue(A, B, bias, stream_k=1)
+    torch.cuda.synchronize()
+    o, m = oracle_run(prob, "rc")
+    check_bound(c1.float().cpu().numpy(), o, m, "split-K")
+    check_bound(dp.float().cpu().numpy(), o, m, "data-parallel")
+
+
+@pytest.mark.parametrize("variant", ["f32_out", "col_bias", "prologue", "batched", "gemm2", "sigmoid"])
+def test_split_k_variants(variant):
+    """Split-K composes with fp32 output, COL bias, the prologue transform, batching, the sum of
+    matmuls and a non-ReLU root op (exact on small integers / within the bound)."""
+    M, N, K = 384, 640, 3072
+    if variant == "prologue":
+        prob = workloads.make_problem(M, N, K, seed=47, kind="smallint", bias_mode="row", prologue="scale_k")
+        assert ge.plan(M, N, K, layouts="rc", prologue="scale_k")["split_k"] > 1
+        got = run_gpu(prob, "rc")
+        out, _ = oracle_run(prob, "rc")
+        assert np.array_equal(got, exact_expect(out, torch.float16))
+    elif variant in ("f32_out", "col_bias", "sigmoid"):
+        bm = "col" if variant == "col_bias" else "row"
+        kind = "uniform" if variant == "sigmoid" else "smallint"
+        prob = workloads.make_problem(M, N, K, seed=48, kind=kind, bias_mode=bm)
+        dt = torch.float32 if variant == "f32_out" else torch.float16
+        op = "bias_sigmoid" if variant == "sigmoid" else None
+        got = run_gpu(prob, "rc", out_dtype=dt, op=op)
+        out, mag = oracle_run(prob, "rc", act="sigmoid" if variant == "sigmoid" else "default")
+        if variant == "sigmoid":
+            check_bound(got, out, mag, "split-K sigmoid")
+        else:
+            assert np.array_equal(got, exact_expect(out, dt))
+    elif variant == "batched":
+        batch = 3
+        assert ge.plan(M, N, K, batch=batch, layouts="rr")["split_k"] > 1
+        probs = [workloads.make_problem(M, N, K, seed=49 + i, kind="smallint", bias_mode="row") for i in range(batch)]
+        A = torch.stack([q.A for q in probs]).cuda()
+        B = torch.stack([q.B for q in probs]).cuda()
+        bias = torch.stack([q.bias for q in probs]).cuda()
+        C = ge.gemm_epilogue_batched(A, B, bias)
+        torch.cuda.synchronize()
+        for i, q in enumerate(probs):
+            out, _ = oracle_run(q, "rr")
+            assert np.array_equal(C[i].float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+    else:
+        K1, K2 = 1536, 1536
+        p1 = workloads.make_problem(M, N, K1, seed=52, kind="smallint", bias_mode="row")
+        p2 = workloads.make_problem(M, N, K2, seed=53, kind="smallint", bias_mode="row")
+        C = ge.gemm2_epilogue(p1.A.cuda(), p1.B.cuda(), p2.A.cuda(), p2.B.cuda(), p1.bias.cuda())
+        torch.cuda.synchronize()
+        out, _ = oracle.gemm2_epilogue(p1.A, p1.B, p2.A, p2.B, M, N, K1, K2, bias=p1.bias, bias_mode="row")
+        assert np.array_equal(C.float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+
+
 # ------------------------------------------------------------------ the paper's pointwise op set
 OPS = {"sigmoid": (None, False), "bias_sigmoid": ("sigmoid", False), "tanh": (None, False),
        "bias_tanh": ("tanh", False), "sub_bias": (None, True), "sub_bias_relu": ("relu", True),
