@@ -134,6 +134,10 @@ def _workspace(device, stream_handle):
     launch leaves it zero-filled."""
     key = (device.index if hasattr(device, "index") else int(device), int(stream_handle))
     ws = _workspaces.get(key)
+    if ws is None and torch.cuda.is_current_stream_capturing():
+        # allocating here would capture its zero-fill into the graph (replayed every time): no
+        # workspace, so the library plans without stream-K (split-K needs none)
+        return None
     if ws is None:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
         ws = torch.zeros(sms * (128 * 256 * 4 + 8), dtype=torch.uint8, device=device)

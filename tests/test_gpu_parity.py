@@ -235,11 +235,14 @@ def test_stream_k_deterministic_repeated_and_graph():
     A, B = dev_operands(prob, "rc")
     bias = prob.bias.cuda()
     kw = dict(bias_mode="col", tile_n=256, cta_group=2, stream_k=2)
-    c1 = ge.gemm_epilogue(A, B, bias, **kw)
-    c2 = ge.gemm_epilogue(A, B, bias, **kw)
+    cs = torch.cuda.Stream()          # the workspace is per (device, stream) and never allocated
+    with torch.cuda.stream(cs):       # while capturing: create it with an eager launch first
+        c1 = ge.gemm_epilogue(A, B, bias, **kw)
+        c2 = ge.gemm_epilogue(A, B, bias, **kw)
+    cs.synchronize()
     out = torch.empty_like(c1)
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    with torch.cuda.graph(g, stream=cs):
         ge.gemm_epilogue(A, B, bias, out=out, **kw)
     for _ in range(3):
         out.zero_()
