@@ -68,7 +68,12 @@ typedef enum {
     GE_EPI_BIAS_SIGMOID = 5,
     GE_EPI_TANH = 8,        /* activation flag: tanh(v)                                      */
     GE_EPI_BIAS_TANH = 9,
-    GE_EPI_SUB = 16         /* modifier: subtract the bias (v = A.B - beta); needs GE_EPI_BIAS */
+    GE_EPI_SUB = 16,        /* modifier: subtract the bias (v = A.B - beta); needs GE_EPI_BIAS */
+    GE_EPI_F16_INTERMEDIATE = 32 /* modifier: the paper-literal rounding point (PAPER.md:1109-1112,
+                               1119-1122; DESIGN.md R-C3): the fp32 accumulator is rounded to fp16
+                               (RNE) before the pointwise op and acc16 +- beta is rounded to fp16
+                               again before the activation, i.e. act(fp16(fp16(acc) +- beta)).
+                               Default (flag clear): fp32 throughout, one rounding at the store. */
 } ge_epilogue_op;
 
 /* Shape of the bias operand beta (DESIGN.md R-C2). */

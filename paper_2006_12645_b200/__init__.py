@@ -43,6 +43,7 @@ class Status:
 
 EPI = {"none": 0, "bias": 1, "relu": 2, "bias_relu": 3, "sigmoid": 4, "bias_sigmoid": 5, "tanh": 8, "bias_tanh": 9,
        "sub_bias": 17, "sub_bias_relu": 19, "sub_bias_sigmoid": 21, "sub_bias_tanh": 25}
+EPI_F16_INTERMEDIATE = 32
 BIAS_MODE = {"row": 0, "col": 1, "full": 2}
 PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
 
@@ -185,8 +186,12 @@ def _stream(stream, device_index: Optional[int] = None) -> int:
 
 
 def _op(op: str, bias) -> int:
+    """op name -> ge_epilogue_op flags; a "literal_" prefix (e.g. "literal_bias_relu") selects the
+    paper-literal rounding point act(fp16(fp16(acc) +- bias)) (GE_EPI_F16_INTERMEDIATE, DESIGN.md R-C3)."""
     if op is None:
         op = "bias_relu" if bias is not None else "relu"
+    if op.startswith("literal_"):
+        return EPI[op[len("literal_"):]] | EPI_F16_INTERMEDIATE
     return EPI[op]
 
 
@@ -211,7 +216,8 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     A: (M, K) fp16, B: (K, N) fp16, row- or column-major views.  bias: (N,) for bias_mode "row",
     (M,) for "col", (M, ldbias>=N) row-major for "full".  op in {"none", "bias", "relu", "bias_relu",
     "sigmoid", "bias_sigmoid", "tanh", "bias_tanh", "sub_bias", "sub_bias_relu", "sub_bias_sigmoid",
-    "sub_bias_tanh"} (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32) or "relu".
+    "sub_bias_tanh"}, each optionally prefixed "literal_" for the paper-literal fp16 rounding of the
+    intermediate (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32) or "relu".
     Returns C (M, N) row-major in out_dtype (fp16 or fp32), asynchronously on the current stream.
     """
     lib = load_library()

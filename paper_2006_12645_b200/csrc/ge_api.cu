@@ -97,9 +97,10 @@ bool overlap(const void* a, int64_t na, const void* b, int64_t nb) {
 }
 
 // op bit flags (include/gemm_epilogue.h): bit 0 bias, bit 1 ReLU, bit 2 Sigmoid, bit 3 Tanh,
-// bit 4 subtract the bias; at most one activation, subtraction only with a bias.
+// bit 4 subtract the bias, bit 5 paper-literal fp16 rounding of the intermediate; at most one
+// activation, subtraction only with a bias.
 bool op_valid(int32_t op) {
-    if (op < 0 || op > 31) return false;
+    if (op < 0 || op > 63) return false;
     const int acts = ((op >> 1) & 1) + ((op >> 2) & 1) + ((op >> 3) & 1);
     return acts <= 1 && (!(op & GE_EPI_SUB) || (op & GE_EPI_BIAS));
 }
@@ -533,6 +534,7 @@ ge_status launch(Args& a, cudaStream_t st) {
                  (a.o.bias_mode != GE_BIAS_FULL || a.o.ldbias % 8 == 0);
     p.act = act_of(a.op);
     p.bias_sign = (a.op & GE_EPI_SUB) ? -1.0f : 1.0f;
+    p.literal = (a.op & GE_EPI_F16_INTERMEDIATE) ? 1 : 0;
     p.scale = a.o.prologue == GE_PRO_SCALE_K ? a.o.prologue_scale : nullptr;
     p.prologue = a.o.prologue;
     p.scale_vec = p.scale && (reinterpret_cast<uintptr_t>(p.scale) % 16 == 0);

@@ -72,6 +72,7 @@ struct Params {
     long long ldbias, stride_bias;
     int act;                        // ACT_* applied at the root of the epilogue
     float bias_sign;                // +1 add, -1 subtract the bias
+    int literal;                    // paper-literal rounding point (DESIGN.md R-C3): fp16(fp16(acc) +- bias)
     // prologue
     const float* scale;
     int prologue;                   // PRO_*
@@ -616,6 +617,14 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 float f[W];
 #pragma unroll
                 for (int e = 0; e < W; ++e) f[e] = __uint_as_float(v[e]);
+                // paper-literal reading: the accumulator is converted to fp16
+                // before the pointwise op, and the fp16 add rounds again (fp32 add + RNE to fp16 is
+                // the correctly rounded fp16 sum: 24 >= 2*11 + 2 bits, no double-rounding error)
+                auto to_f16 = [&]() {
+#pragma unroll
+                    for (int e = 0; e < W; ++e) f[e] = __half2float(__float2half_rn(f[e]));
+                };
+                if (p.literal) to_f16();
                 if (p.bias_mode == BIAS_ROW) {
                     const uint4* bs = reinterpret_cast<const uint4*>(smem_bias + c * W);     // broadcast reads
 #pragma unroll
@@ -657,6 +666,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
                     for (int e = 0; e < W; ++e) f[e] += bsg * bv;
                 }
+                if (p.literal && p.bias_mode != BIAS_NONE) to_f16();
                 activate(f, W, p.act);
                 if constexpr (OUT_F32) {
 #pragma unroll

@@ -102,7 +102,9 @@ def test_validate_invalid_values(lib, ge):
     assert v(lib, la=2) == S.INVALID_VALUE
     assert v(lib, op=6) == S.INVALID_VALUE             # two activations
     assert v(lib, op=16) == S.INVALID_VALUE            # subtract without a bias
-    assert v(lib, op=32) == S.INVALID_VALUE
+    assert v(lib, op=64) == S.INVALID_VALUE
+    assert v(lib, op=32 | 3) == 0 and v(lib, op=32 | 2) == 0   # paper-literal rounding modifier (R-C3)
+    assert v(lib, op=32 | 6) == S.INVALID_VALUE
     assert v(lib, op=4) == 0 and v(lib, op=9) == 0 and v(lib, op=25) == 0
     assert v(lib, lda=32) == S.INVALID_VALUE            # row-major A needs lda >= K = 64
     assert v(lib, la=1, lda=64) == S.INVALID_VALUE      # col-major A needs lda >= M = 128

@@ -441,3 +441,48 @@ def test_host_entry_batched_items():
     Cd = ge.gemm_epilogue_batched(A.cuda(), B.cuda(), bias.cuda(), **kw)
     torch.cuda.synchronize()
     assert torch.equal(Ch, Cd.cpu())
+
+
+# ------------------------------------------------------------------ paper-literal rounding point (R-C3)
+def _eighths_problem(M, N, K, seed):
+    """a = u/64, bias = v/64 (u, v ~ U{-255..255}), b ~ U{-3..3}: every product and partial sum is
+    exact in fp32 (<= 17 significant bits) but generally NOT representable in fp16, so the
+    paper-literal fp16 rounding of the accumulator changes results while
+    staying exactly computable on both sides."""
+    g = torch.Generator().manual_seed(seed)
+    A = (torch.randint(-255, 256, (M, K), generator=g).double() / 64).half()
+    B = torch.randint(-3, 4, (K, N), generator=g).half()
+    bias = (torch.randint(-255, 256, (N,), generator=g).double() / 64).half()
+    return workloads.Problem(M, N, K, A, B, bias, None, {"bias_mode": "row", "prologue": None})
+
+
+@pytest.mark.parametrize("tile_n,cg", [(512, 2), (256, 2), (128, 1)])
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.float32])
+def test_literal_rounding_point(tile_n, cg, out_dtype):
+    """GE_EPI_F16_INTERMEDIATE: relu(fp16(fp16(acc) + bias)) (DESIGN.md R-C3).  On data whose fp32
+    accumulation is exact the GPU equals the oracle's literal reading bitwise, and the flag is
+    observable (it differs from the default single-rounding result somewhere); on uniform data
+    both readings stay within the north_star bound."""
+    prob = _eighths_problem(300, 520, 96, seed=61)
+    got = run_gpu(prob, "rr", op="literal_bias_relu", out_dtype=out_dtype, tile_n=tile_n, cta_group=cg)
+    lit, _ = oracle_run(prob, "rr", literal_round=True)
+    assert np.array_equal(got, exact_expect(lit, out_dtype))
+    default = run_gpu(prob, "rr", op="bias_relu", out_dtype=out_dtype, tile_n=tile_n, cta_group=cg)
+    assert not np.array_equal(got, default)
+    uni = workloads.make_problem(200, 300, 700, seed=62, kind="uniform", bias_mode="row")
+    got_u = run_gpu(uni, "rc", op="literal_bias_relu", out_dtype=out_dtype, tile_n=tile_n, cta_group=cg)
+    out, mag = oracle_run(uni, "rc")
+    check_bound(got_u, out, mag, "literal vs exact")
+
+
+def test_literal_rounding_split_k_and_no_bias():
+    """The literal rounding happens once, after the full K reduction (split-K shapes), and with no
+    bias it reduces to act(fp16(acc))."""
+    prob = _eighths_problem(128, 256, 64 * 40, seed=63)
+    got = run_gpu(prob, "rr", op="literal_bias_relu")
+    lit, _ = oracle_run(prob, "rr", literal_round=True)
+    assert np.array_equal(got, exact_expect(lit, torch.float16))
+    nob = workloads.Problem(prob.M, prob.N, prob.K, prob.A, prob.B, None, None, {"bias_mode": None, "prologue": None})
+    got = run_gpu(nob, "rr", op="literal_relu", out_dtype=torch.float32)
+    lit, _ = oracle_run(nob, "rr", literal_round=True)
+    assert np.array_equal(got, lit)
