@@ -109,7 +109,11 @@ typedef struct {
                                        per-device buffer (then stream-K launches on different streams of
                                        one device must not run concurrently; stream_k = 1 disables it). */
     int64_t workspace_bytes;
-} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0} */
+    int32_t multicast;              /* 0 = heuristic; 1 = off; 2 = force clusters of two CTA pairs stacked
+                                       along M (512 x tile_n tiles) whose B tiles are loaded once and
+                                       TMA-multicast to both pairs (a third less L2->SM traffic per flop;
+                                       needs no prologue and stream_k != 2; data-parallel tiles only) */
+} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0} */
 
 typedef enum {
     GE_OK = 0,

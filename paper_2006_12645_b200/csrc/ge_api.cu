@@ -132,6 +132,10 @@ ge_status validate(Args& a) {
     if (o.cta_group == 2 && o.tile_n == 192 && a.lb == GE_ROW_MAJOR)
         return fail(GE_ERR_INVALID_VALUE, "tile_n 192 with cta_group 2 needs a column-major (K-major) B");
     if (o.stream_k < 0 || o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
+    if (o.multicast < 0 || o.multicast > 2) return fail(GE_ERR_INVALID_VALUE, "multicast must be 0, 1 or 2");
+    if (o.multicast == 2 && (o.prologue != GE_PRO_NONE || o.stream_k == 2 || (o.cta_group && o.cta_group != 2) ||
+                             (o.tile_n && o.tile_n != 256 && o.tile_n != 512)))
+        return fail(GE_ERR_INVALID_VALUE, "multicast = 2 needs no prologue, stream_k != 2, cta_group 0/2, tile_n 0/256/512");
     if (o.workspace_bytes < 0 || (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 15)))
         return fail(GE_ERR_INVALID_VALUE, "workspace must be 16-byte aligned with a non-negative size");
     // packed defaults
@@ -211,6 +215,7 @@ ge_status validate(Args& a) {
 // ------------------------------------------------------------------ plan
 struct Plan {
     int bn, cg, stages;
+    bool mc = false;       // multicast cluster of two CTA pairs (tile 512 x bn, B shared by TMA multicast)
     int64_t tiles;
     int64_t sk_tiles;      // tiles of the last, partial wave split stream-K across all clusters (0 = none)
     int64_t clusters;      // persistent clusters launched
@@ -224,8 +229,24 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // (operand bytes per MMA flop double), the CTA pair halves per-SM B traffic, and the 256 x 512
 // pair tile moves the least operand data per flop (L2 and HBM) at the cost of a single,
 // non-double-buffered accumulator (its drain is partly exposed: kExposedK below).
+// Multicast clusters of two pairs read a third less operand data from L2 per flop (B is shared).
+// Measured on B200 (profiles/r01_tune_sweep.json, rotating operands): 256 x 256 pair tiles in
+// multicast clusters gain 3-4% on long-K shapes whose wave count the 33 co-resident 4-CTA clusters
+// (132 SMs) do not raise, and lose ~2% at K = 2048 (fixed per-tile cost kMcFixed); the 512-wide
+// multicast tile never measured best, so the heuristic leaves it to explicit requests.
+double config_eff_mc(int bn) {
+    static const double env = [] {
+        const char* e = getenv("GE_MC_EFF");                // calibration override (tuning only)
+        return e ? atof(e) : 0.0;
+    }();
+    if (env > 0) return env;
+    return bn == 512 ? 1.06 : 1.04;
+}
+constexpr double kMcFixed = 1050.0;     // cycles per multicast tile (cluster-of-4 pipeline fill/drain)
+constexpr double kDrain512 = 13600.0;   // cycles exposed per 256 x 512 pair tile (single accumulator)
+
 double config_eff(int bn, int cg) {
-    if (cg == 2) return bn == 512 ? 1.06 : bn == 256 ? 1.00 : bn == 192 ? 0.87 : 0.58;
+    if (cg == 2) return bn == 512 ? 1.20 : bn == 256 ? 1.00 : bn == 192 ? 0.87 : 0.58;
     return bn == 256 ? 0.92 : bn == 192 ? 0.82 : bn == 128 ? 0.52 : 0.30;
 }
 
@@ -236,6 +257,7 @@ double config_eff(int bn, int cg) {
 // planner then uses its GPC estimate).
 struct SplitCap {
     int cap[4][9];
+    int mc[2];          // co-resident multicast clusters (two CTA pairs) for BN = 512, 256
 };
 std::mutex g_cap_mu;
 SplitCap g_cap[64];
@@ -252,6 +274,8 @@ const SplitCap* split_capacity() {
         const int bns[4] = {64, 128, 192, 256};
         for (int i = 0; i < 4; ++i)
             for (int S = 0; S <= 8; ++S) c.cap[i][S] = S >= 2 ? ge::clusters_cg1(bns[i], S) : 0;
+        c.mc[0] = ge::clusters_mc(512);
+        c.mc[1] = ge::clusters_mc(256);
         g_cap_done[dev & 63] = true;
         if (getenv("GE_PRINT_SPLIT_CAPACITY"))      // dev: calibration of the planner's fallback estimate
             for (int i = 0; i < 4; ++i)
@@ -291,7 +315,9 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
         // time per stage than 256 x 512 pair tiles become shared-memory bound.
         if (a.o.prologue != GE_PRO_NONE && bn * cg < 1024) eff *= 0.55;
         const double t_kb = 128.0 * bn * 64 * 2 / (8192.0 * eff);
-        const double drain = bn == 512 ? 3.0 * t_kb : 0.0;          // exposed per tile (single acc)
+        // exposed per tile by the single 512-column accumulator (drain + refill), fitted with eff = 1.20
+        // to the 256 x 256 / 256 x 512 ratios measured at 4096^3 and 8192^3 (profiles/r01_tune_sweep.json)
+        const double drain = bn == 512 ? kDrain512 : 0.0;
         const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
         double cost = waves * (nkb * t_kb + drain);
         int64_t sk = 0;
@@ -338,13 +364,37 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
                 }
             }
         }
+        if (a.o.multicast == 2) cost = 1e300;                      // forced multicast: pairs only below
         if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
-            best = Plan{bn, cg, ge::stages_for(bn, cg), tiles, sk, sk ? conc : std::min<int64_t>(tiles, conc)};
+            best = Plan{bn, cg, ge::stages_for(bn, cg), false, tiles, sk, sk ? conc : std::min<int64_t>(tiles, conc)};
             if (splits) {
                 best.splits = splits;
                 best.clusters = tiles * splits;
             }
             best_cost = cost;
+        }
+    }
+    // Multicast clusters of two CTA pairs: data-parallel tiles of
+    // 512 x BN, co-resident clusters from cudaOccupancyMaxActiveClusters (GPC-bound: 4-CTA clusters
+    // leave some SMs idle, which the cost model charges through `conc`).
+    const bool mc_ok = a.o.multicast != 1 && a.o.prologue == GE_PRO_NONE && a.o.stream_k != 2 &&
+                       (!a.o.cta_group || a.o.cta_group == 2) && (a.M > 256 || a.o.multicast == 2);
+    if (mc_ok) {
+        for (const int bn : {512, 256}) {
+            if (a.o.tile_n && a.o.tile_n != bn) continue;
+            if (bn == 512 && a.o.multicast != 2) continue;        // never measured best (see config_eff_mc)
+            const int64_t tiles = a.batch * cdiv(a.M, 512) * cdiv(a.N, bn);
+            int64_t conc = (cap && cap->mc[bn == 512 ? 0 : 1] > 0) ? cap->mc[bn == 512 ? 0 : 1]
+                                                                    : static_cast<int64_t>(33 * (sms / 148.0));
+            conc = std::max<int64_t>(1, conc);
+            const double t_kb = 128.0 * bn * 64 * 2 / (8192.0 * config_eff_mc(bn));
+            const double drain = bn == 512 ? kDrain512 : 0.0;
+            const double cost = static_cast<double>(cdiv(tiles, conc)) * (nkb * t_kb + drain + kMcFixed);
+            if (a.o.multicast == 2 || cost < best_cost * (1 - 1e-9)) {
+                if (a.o.multicast == 2 && best.mc && cost >= best_cost) continue;
+                best = Plan{bn, 2, ge::stages_for(bn, 2), true, tiles, 0, std::min<int64_t>(tiles, conc)};
+                best_cost = cost;
+            }
         }
     }
     best.clusters = std::max<int64_t>(best.clusters, 1);
@@ -481,7 +531,8 @@ ge_status launch(Args& a, cudaStream_t st) {
         if (!a_mn) ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.K, a.M, a.batch, a.lda, a.sA, 64, 128);
         else ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.M, a.K, a.batch, a.lda, a.sA, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for A");
-        const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg);   // B rows per MMA per CTA
+        // B rows per MMA per CTA; multicast clusters load (and multicast) half of them per CTA
+        const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg / (pl.mc ? 2 : 1));
         if (!b_mn) ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.K, a.N, a.batch, a.ldb, a.sB, 64, brows);
         else ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.N, a.K, a.batch, a.ldb, a.sB, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for B");
@@ -491,7 +542,7 @@ ge_status launch(Args& a, cudaStream_t st) {
         if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.K2, a.M, 1, a.ldp, 0, 64, 128);
         else ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.M, a.K2, 1, a.ldp, 0, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for P");
-        const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg);
+        const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg / (pl.mc ? 2 : 1));
         if (!b_mn) ok = encode3d(&maps.q, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.Q, a.K2, a.N, 1, a.ldq, 0, 64, brows);
         else ok = encode3d(&maps.q, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.Q, a.N, a.K2, 1, a.ldq, 0, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for Q");
@@ -509,7 +560,7 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.N = static_cast<int>(a.N);
     p.K = static_cast<int>(a.K);
     p.batch = static_cast<int>(a.batch);
-    p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg));
+    p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg * (pl.mc ? 2 : 1)));
     p.num_n_tiles = static_cast<int>(cdiv(a.N, pl.bn));
     p.num_k_blocks1 = static_cast<int>(cdiv(a.K, ge::kBK));
     p.num_k_blocks = p.num_k_blocks1 + static_cast<int>(cdiv(a.K2, ge::kBK));
@@ -576,9 +627,12 @@ ge_status launch(Args& a, cudaStream_t st) {
             plan.clusters = std::min<int64_t>(plan.tiles, sms / plan.cg);     // data-parallel fallback
         }
     }
-    const int grid = static_cast<int>(std::max<int64_t>(plan.clusters, 1) * plan.cg);
+    const int grid = static_cast<int>(std::max<int64_t>(plan.clusters, 1) * plan.cg * (plan.mc ? 2 : 1));
     cudaError_t e;
-    if (pl.cg == 1) {
+    if (pl.mc) {
+        if (pl.bn == 512) e = ge::launch_cg2_bn512_mc(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg2_bn256_mc(a_mn, b_mn, f32, pro, maps, p, grid, st);
+    } else if (pl.cg == 1) {
         if (pl.bn == 64) e = ge::launch_cg1_bn64(a_mn, b_mn, f32, pro, maps, p, grid, st);
         else if (pl.bn == 128) e = ge::launch_cg1_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
         else if (pl.bn == 192) e = ge::launch_cg1_bn192(a_mn, b_mn, f32, pro, maps, p, grid, st);
@@ -602,7 +656,7 @@ Args make_args(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t la, int32
                int64_t ldc, int64_t sC, int32_t op, const ge_options* opt) {
     Args a{batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op, {}};
     if (opt) a.o = *opt;
-    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0};
+    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0};
     return a;
 }
 
@@ -894,7 +948,7 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
     if (a.o.stream_k < 0 || a.o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
     const Plan p = make_plan(a, num_sms, split_capacity());     // (nullptr without a device)
-    if (tile_m) *tile_m = 128 * p.cg;
+    if (tile_m) *tile_m = 128 * p.cg * (p.mc ? 2 : 1);
     if (tile_n) *tile_n = p.bn;
     if (cta_group) *cta_group = p.cg;
     if (stages) *stages = p.stages;

@@ -1,0 +1,10 @@
+// Instantiates the fused kernel family for BN = 256, CTA pairs in multicast clusters of two pairs
+// (the pairs share B tiles through TMA multicast; no prologue variants).
+#include "ge_launch.cuh"
+
+namespace ge {
+cudaError_t launch_cg2_bn256_mc(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m, const Params& p, int grid,
+                               cudaStream_t st) {
+    return launch_bn_cg<256, 2, true>(a_mn, b_mn, f32, pro, m, p, grid, st);
+}
+}  // namespace ge

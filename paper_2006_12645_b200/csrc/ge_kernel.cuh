@@ -97,7 +97,7 @@ struct Params {
     // diagnostics (GE_DEBUG_STATS): per-CTA blocked-cycle counters, or nullptr
     unsigned long long* dbg;
     int dbg_noload;                 // dev experiment only: stop issuing TMA after the ring is full once
-    int dbg_flags;                  // dev experiments only (GE_DEBUG_FLAGS): 1 skip epilogue, 2 half-major MMA order
+    int dbg_flags;                  // dev experiments only (GE_DEBUG_FLAGS): 1 skip epilogue, 8 no epilogue math, 16 no stores
 };
 
 // Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
@@ -121,7 +121,10 @@ struct Cfg {
     // Epilogue staging buffers per warp (double-buffered TMA stores).
     static constexpr int kStagingBufs = 2;
     static constexpr int kStagingBytes = kStagingBufs * kStagingSetBytes;
-    static constexpr int kBiasBytes = BN * 2;                         // tile's ROW-bias slice (fp16)
+    // tile's ROW-bias slice: fp32 with the bias sign applied (no per-element conversion in the
+    // epilogue) where the smem budget allows it, fp16 for the 256 x 512 pair tile (4 stages need it)
+    static constexpr bool kBiasF32 = BN <= 256;
+    static constexpr int kBiasBytes = BN * (kBiasF32 ? 4 : 2);
     static constexpr int kStagesRaw = (kSmemBudget - 1024 - kStagingBytes - kBiasBytes - kBarBytes) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : (GE_PAIR_RELEASE ? kStagesRaw & ~1 : kStagesRaw);
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStagingBytes + kBiasBytes + kBarBytes;
@@ -257,7 +260,10 @@ __host__ __device__ constexpr int kernel_threads(bool out_f32, bool pro) {
     return 32 * (4 + epi_warps(out_f32, pro) + (pro ? kXformWarps : 0));
 }
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG>
+// MC: clusters of two CTA pairs stacked along M that share the B tile: each CTA loads half of its
+// B block and multicasts it to the CTA at the same position in the other pair (a third less L2->SM
+// operand traffic per flop); data-parallel tiles only (no prologue, stream-K or split-K).
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG, bool MC = false>
 __global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO), 1)
 ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_p,
@@ -280,6 +286,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     uint8_t* smem_b = smem + S * C_::kAStage;
     uint8_t* smem_c = smem_b + S * C_::kBStage;
     __half* smem_bias = reinterpret_cast<__half*>(smem_c + C_::kStagingBytes);
+    float* smem_bias_f = reinterpret_cast<float*>(smem_c + C_::kStagingBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_c + C_::kStagingBytes + C_::kBiasBytes);
     uint64_t* full_bar = bars;                  // [S] TMA -> MMA (or -> transform)
     uint64_t* empty_bar = bars + S;             // [S] MMA -> TMA
@@ -293,8 +300,14 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
-    const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
+    static_assert(!MC || (CG == 2 && !PRO), "multicast clusters: CTA pairs without a prologue");
+    constexpr int CL = MC ? 2 * CG : CG;                 // CTAs per cluster
+    constexpr int TILE_M = C_::kTileM * (MC ? 2 : 1);    // rows of one scheduled tile
+    const uint32_t crank = (CG == 2) ? ptx::cluster_ctarank() : 0;
+    const uint32_t rank = crank & 1;                     // rank inside the CTA pair
+    const uint32_t pair = MC ? (crank >> 1) : 0;         // pair inside a multicast cluster
     const bool leader = rank == 0;
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pair));
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmap_a);
@@ -310,7 +323,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier and
             // only the leader's producer arrives (expecting both CTAs' bytes).
             ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], MC ? 2 : 1);      // MC: both pairs' MMAs read stage s's B
             ptx::mbar_init(&xform_bar[s], kXformWarps * CG);
         }
         for (int b = 0; b < 2; ++b) ptx::mbar_init(&tfull_bar[b], 1);
@@ -337,8 +350,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
     for (int i = 0; i < DBG_SLOTS; ++i) dl[i] = 0;
     const long long t_start = clock64();
-    const int cluster_id = blockIdx.x / CG;
-    const int num_clusters = gridDim.x / CG;
+    const int cluster_id = blockIdx.x / CL;
+    const int num_clusters = gridDim.x / CL;
     const int nkb = p.num_k_blocks;
     const WorkSeq work(p, cluster_id, num_clusters);
 
@@ -353,8 +366,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const Piece pc = work.get(wi);
                 const long long t = pc.tile;
                 int b, mt, nt;
-                decode_tile(p, t, C_::kTileM, b, mt, nt);
-                const int m0 = mt * C_::kTileM + rank * kRowsPerCta;
+                decode_tile(p, t, TILE_M, b, mt, nt);
+                const int m0 = mt * TILE_M + pair * C_::kTileM + rank * kRowsPerCta;
                 const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                     // paired release: the MMA warp commits only the odd stage of each pair (that
@@ -396,7 +409,17 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     for (int h = 0; h < NH; ++h) {
                         uint8_t* sbh = sb + h * C_::kBBlockBytes;
                         const int nh = n0 + h * C_::kUmmaN;
-                        if constexpr (B_MN) {
+                        if constexpr (MC) {
+                            // this CTA's 64-row half `pair` of the block, to both pairs' CTAs of rank `rank`
+                            // (an MN-major half is one 64-wide swizzle atom; the K-major map's box is 64 rows)
+                            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
+                            if constexpr (B_MN)
+                                ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], nh + pair * 64, k0, b,
+                                                         mask, pol_b);
+                            else
+                                ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], k0, nh + pair * 64, b,
+                                                         mask, pol_b);
+                        } else if constexpr (B_MN) {
 #pragma unroll
                             for (int i = 0; i < C_::kBBlockRows / 64; ++i)
                                 load(sbh + i * 8192, map_b, nh + i * 64, k0, pol_b);
@@ -442,7 +465,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     return b_desc0 + static_cast<uint64_t>((stage * C_::kBStage + h * C_::kBBlockBytes) >> 4);
                 };
                 auto release_stage = [&](int stage) {
-                    if (!GE_PAIR_RELEASE || (stage & 1)) ptx::mma_commit_elect<CG>(&empty_bar[stage]);
+                    // MC: the stage's B halves came from both pairs, so both pairs' producers wait for it
+                    if (!GE_PAIR_RELEASE || (stage & 1)) ptx::mma_commit_elect<CG>(&empty_bar[stage], MC ? 0xF : 0x3);
                 };
                 auto mma_half = [&](int stage, int kb, int h) {
                     ptx::mma_kblock<CG, A_STEP, B_STEP>(d_tmem + h * C_::kUmmaN, desc_a(stage), desc_b(stage, h), IDESC,
@@ -501,7 +525,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             release_stage(st);
                         }
                     }
-                    ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
+                    ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
                 } else {
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                         if (!(GE_EARLY_TEST && next_ready))
@@ -521,7 +545,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         }
                         mma_half(s, kb, 0);
                         release_stage(s);                         // smem slot free once these MMAs finish
-                        if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc]);
+                        if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
                         if (++s == S) { s = 0; phase ^= 1; }
                     }
                 }
@@ -555,10 +579,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             const Piece pc = work.get(it);
             const long long t = pc.tile;
             int b, mt, nt;
-            decode_tile(p, t, C_::kTileM, b, mt, nt);
+            decode_tile(p, t, TILE_M, b, mt, nt);
             const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
             const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
-            const int row0 = mt * C_::kTileM + rank * kRowsPerCta + q * 32;   // first row of this warp
+            const int row0 = mt * TILE_M + pair * C_::kTileM + rank * kRowsPerCta + q * 32;   // first row of this warp
             const int row = row0 + lane;
             const __half* bias_b = p.bias ? p.bias + b * p.stride_bias : nullptr;
             // Bias operands are fetched while this tile's MMAs still run (global loads would miss
@@ -569,7 +593,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 ptx::named_bar_sync(1, EPI_WARPS * 32);            // previous tile's reads are done
                 for (int i = threadIdx.x - 128; i < BN; i += EPI_WARPS * 32) {
                     const int col = nt * BN + i;
-                    smem_bias[i] = col < p.N ? bias_b[col] : __float2half_rn(0.0f);
+                    if constexpr (C_::kBiasF32) smem_bias_f[i] = col < p.N ? p.bias_sign * __half2float(bias_b[col]) : 0.0f;
+                    else smem_bias[i] = col < p.N ? bias_b[col] : __float2half_rn(0.0f);
                 }
                 ptx::named_bar_sync(1, EPI_WARPS * 32);
             }
@@ -606,7 +631,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&tempty_bar[acc * NH + h], 0);
+                    if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&tempty_bar[acc * NH + h], 2 * pair);
                     else ptx::mbar_arrive(&tempty_bar[acc * NH + h]);
                 }
             };
@@ -625,7 +650,17 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     for (int e = 0; e < W; ++e) f[e] = __half2float(__float2half_rn(f[e]));
                 };
                 if (p.literal) to_f16();
-                if (p.bias_mode == BIAS_ROW) {
+                if (C_::kBiasF32 && p.bias_mode == BIAS_ROW) {
+                    const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
+#pragma unroll
+                    for (int g = 0; g < W / 4; ++g) {
+                        const float4 bf = bs[g];
+                        f[4 * g] += bf.x;
+                        f[4 * g + 1] += bf.y;
+                        f[4 * g + 2] += bf.z;
+                        f[4 * g + 3] += bf.w;
+                    }
+                } else if (p.bias_mode == BIAS_ROW) {
                     const uint4* bs = reinterpret_cast<const uint4*>(smem_bias + c * W);     // broadcast reads
 #pragma unroll
                     for (int g = 0; g < W / 8; ++g) {
@@ -765,7 +800,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (o == js) continue;
                         uint32_t v[W];
                         load(c, v);
-                        ptx::tmem_ld_wait();
+                        ptx::tmem_ld_wait_regs(v);
                         const int slot = (4 * c + q - u_lo(o)) * (S - 1) + (js < o ? js : js - 1);
                         const uint32_t dst = ptx::mapa_shared(recv_base + slot * UB + lane * 16, static_cast<uint32_t>(o));
                         const uint32_t rbar = ptx::mapa_shared(ptx::smem_u32(recv_full_bar), static_cast<uint32_t>(o));
@@ -782,7 +817,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (owner(c) != js) continue;
                         uint32_t v[W];
                         load(c, v);
-                        ptx::tmem_ld_wait();
+                        ptx::tmem_ld_wait_regs(v);
                         const uint8_t* rb = smem_a + (4 * c + q - u_lo(js)) * (S - 1) * UB + lane * 16;
 #pragma unroll 1
                         for (int s2 = 0; s2 < S - 1; ++s2) {
@@ -814,7 +849,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         const int c = j * NG + grp;
                         uint32_t v[W];
                         load(c, v);
-                        ptx::tmem_ld_wait();
+                        ptx::tmem_ld_wait_regs(v);
                         if (j == CPH - 1) release(0);
                         float4* dst = ws_slot(cluster_id) + static_cast<size_t>(c * (W / 4)) * kRowsPerCta + trow;
 #pragma unroll
@@ -875,7 +910,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         uint32_t v[W];
                         const long long tl0 = (dbg && e_idx == 0) ? clock64() : 0;
                         load(h * CPH_ALL + j * NG + grp, v);
-                        if (nkb > 0) ptx::tmem_ld_wait();
+                        if (nkb > 0) ptx::tmem_ld_wait_regs(v);
                         const long long tl1 = (dbg && e_idx == 0) ? clock64() : 0;
                         if (j == CPH - 1) release(h);
                         compute(h * CPH_ALL + j * NG + grp, v, packed[j]);
@@ -892,12 +927,18 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         const int c = h * CPH_ALL + j * NG + grp;
                         uint32_t v[W];
                         load(c, v);
-                        if (nkb > 0) ptx::tmem_ld_wait();
+                        if (nkb > 0) ptx::tmem_ld_wait_regs(v);
                         if (j == CPH - 1) release(h);
                         if (pc.kind == PIECE_OWNER) add_partials(c, v);
                         uint32_t w[NWORD];
-                        compute(c, v, w);
-                        store(c, w);
+                        if (p.dbg_flags & 8) {      // timing experiment: no epilogue math
+#pragma unroll
+                            for (int e = 0; e < NWORD; ++e) w[e] = v[e];
+                        } else {
+                            compute(c, v, w);
+                        }
+                        if (!(p.dbg_flags & 16)) store(c, w);   // 16: timing experiment, no stores
+                        else if (p.dbg && w[0] == 0x12345678u && w[NWORD - 1] == 0x9abcdef0u) p.dbg[0] = 1;
                     }
                 }
             }

@@ -18,9 +18,9 @@ struct Maps {
 int smem_bytes_for(int bn, int cg);
 int stages_for(int bn, int cg);
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG>
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG, bool MC = false>
 cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st) {
-    auto kern = ge_fused_kernel<BN, A_MN, B_MN, OUT_F32, PRO, CG>;
+    auto kern = ge_fused_kernel<BN, A_MN, B_MN, OUT_F32, PRO, CG, MC>;
     constexpr int smem = Cfg<BN, CG>::kSmemBytes;
     static bool attr_done = false;   // benign race: setting the attribute twice is harmless
     if (!attr_done) {
@@ -36,7 +36,8 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     // CTA pairs; or, for split-K single-CTA tiles, one cluster per tile of `splits` CTAs (K-slices)
-    attr[0].val.clusterDim.x = (CG == 1 && p.splits > 1) ? p.splits : CG;
+    // (MC: two CTA pairs sharing B tiles by TMA multicast)
+    attr[0].val.clusterDim.x = MC ? 2 * CG : (CG == 1 && p.splits > 1) ? p.splits : CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     // programmatic dependent launch: the kernel's prologue may overlap the previous kernel's tail
@@ -54,9 +55,9 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
 
 // Co-resident clusters of `cluster` CTAs of the (BN, CG) kernel on the current device (0 if the
 // query fails); the split-K planner uses it (cluster scheduling is GPC-bound, not SM-count-bound).
-template <int BN, int CG>
+template <int BN, int CG, bool MC = false>
 int max_active_clusters(int cluster) {
-    auto kern = ge_fused_kernel<BN, false, false, false, false, CG>;
+    auto kern = ge_fused_kernel<BN, false, false, false, false, CG, MC>;
     constexpr int smem = Cfg<BN, CG>::kSmemBytes;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
@@ -82,7 +83,7 @@ int max_active_clusters(int cluster) {
 }
 
 // Dispatch over the 16 (A_MN, B_MN, OUT_F32, PRO) variants of one (BN, CG) configuration.
-template <int BN, int CG>
+template <int BN, int CG, bool MC = false>
 cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m, const Params& p, int grid,
                          cudaStream_t st) {
     const int key = (a_mn ? 8 : 0) | (b_mn ? 4 : 0) | (f32 ? 2 : 0) | (pro ? 1 : 0);
@@ -91,8 +92,8 @@ cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m
 // count; an MN-major B stage is built from 64-column swizzle atoms.)
 #define GE_CASE(K, AM, BM, F, P)                                                  \
     case K:                                                                       \
-        if constexpr (BM && BN == 192 && CG == 2) return cudaErrorInvalidValue;   \
-        else return launch_one<BN, AM, BM, F, P, CG>(m, p, grid, st);
+        if constexpr ((BM && BN == 192 && CG == 2) || (MC && P)) return cudaErrorInvalidValue; \
+        else return launch_one<BN, AM, BM, F, P, CG, MC>(m, p, grid, st);
         GE_CASE(0, false, false, false, false)
         GE_CASE(1, false, false, false, true)
         GE_CASE(2, false, false, true, false)
@@ -128,5 +129,8 @@ cudaError_t launch_cg1_bn256(bool, bool, bool, bool, const Maps&, const Params&,
 cudaError_t launch_cg2_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn512(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn512_mc(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256_mc(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+int clusters_mc(int bn);     // co-resident 4-CTA multicast clusters of the (bn, pair) kernel
 
 }  // namespace ge

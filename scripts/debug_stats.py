@@ -6,11 +6,12 @@ import torch
 import paper_2006_12645_b200 as ge
 M, N, K = (int(x) for x in sys.argv[1:4]); lay = sys.argv[4]; bn, cg = int(sys.argv[5]), int(sys.argv[6])
 sk = int(sys.argv[7]) if len(sys.argv) > 7 else 0
+mc = int(sys.argv[8]) if len(sys.argv) > 8 else 0
 A = torch.randn(M, K, device="cuda", dtype=torch.float16); B = torch.randn(K, N, device="cuda", dtype=torch.float16)
 if lay[0] == "c": A = A.t().contiguous().t()
 if lay[1] == "c": B = B.t().contiguous().t()
 bias = torch.randn(N, device="cuda", dtype=torch.float16); C = torch.empty(M, N, device="cuda", dtype=torch.float16)
-for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk)
+for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk, multicast=mc)
 torch.cuda.synchronize()
 st = ge.debug_stats()
 lead = [s for i, s in enumerate(st) if (cg == 1 or i % 2 == 0) and s["total"] > 0]   # active leaders

@@ -2,7 +2,7 @@
 Each candidate runs graph-replayed for ~SECS seconds with rotating operand sets while a thread
 samples NVML; reports TF/s, median SM MHz, median W, and flop/clk/SM (clock-normalised
 efficiency: 8192 = the tensor pipe's dense fp16 rate).
-usage: power_cmp.py M N K [secs] [cfg ...]   cfg = auto | cublas | lt | BNxCG"""
+usage: power_cmp.py M N K [secs] [cfg ...]   cfg = auto | cublas | lt | BNxCG[m]"""
 import sys, os, time, threading, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -28,8 +28,9 @@ def call(cfg, A, B):
         return torch.matmul(A, B, out=C)
     if cfg == "auto":
         return ge.gemm_epilogue(A, B, bias, out=C)
-    bn, cg = (int(x) for x in cfg.split("x"))
-    return ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg)
+    mc = 2 if cfg.endswith("m") else 1          # "512x2m": multicast clusters of two pairs
+    bn, cg = (int(x) for x in cfg.rstrip("m").split("x"))
+    return ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, multicast=mc)
 
 
 flop = 2 * M * N * K

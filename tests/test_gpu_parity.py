@@ -486,3 +486,64 @@ def test_literal_rounding_split_k_and_no_bias():
     got = run_gpu(nob, "rr", op="literal_relu", out_dtype=torch.float32)
     lit, _ = oracle_run(nob, "rr", literal_round=True)
     assert np.array_equal(got, lit)
+
+
+# ------------------------------------------------------------------ multicast clusters of two CTA pairs
+@pytest.mark.parametrize("tile_n", [512, 256])
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_multicast_clusters_exact(tile_n, layouts):
+    """Clusters of two CTA pairs sharing B by TMA multicast (512 x tile_n tiles): bitwise exact on
+    small integers and within the bound on uniform data, with a ragged M whose last cluster tile
+    leaves the second pair entirely out of range (rows 768.. of M = 700) and ragged N, K."""
+    for kind in ("smallint", "uniform"):
+        prob = workloads.make_problem(700, 600, 200, seed=71, kind=kind, bias_mode="row")
+        got = run_gpu(prob, layouts, tile_n=tile_n, cta_group=2, multicast=2)
+        out, mag = oracle_run(prob, layouts)
+        if kind == "smallint":
+            assert np.array_equal(got, exact_expect(out, torch.float16))
+        else:
+            check_bound(got, out, mag, f"mc {tile_n} {layouts}")
+
+
+@pytest.mark.parametrize("variant", ["f32_col", "full_bias", "batched", "gemm2", "long_k"])
+def test_multicast_variants(variant):
+    """fp32 output with a column bias, a full M x N bias, strided batches, the sum of matmuls and a
+    long K (many ring wraps) through the multicast configuration, bitwise exact on small integers."""
+    if variant == "batched":
+        probs = [workloads.make_problem(600, 520, 136, seed=80 + b, kind="smallint", bias_mode="row") for b in range(3)]
+        A = torch.stack([p.A for p in probs]).cuda()
+        B = torch.stack([p.B for p in probs]).cuda()
+        bias = torch.stack([p.bias for p in probs]).cuda()
+        C = ge.gemm_epilogue_batched(A, B, bias, tile_n=512, cta_group=2, multicast=2)
+        torch.cuda.synchronize()
+        for b, p in enumerate(probs):
+            out, _ = oracle_run(p, "rr")
+            assert np.array_equal(C[b].float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+        return
+    if variant == "gemm2":
+        p1 = workloads.make_problem(1100, 700, 96, seed=90, kind="smallint", bias_mode="row")
+        p2 = workloads.make_problem(1100, 700, 160, seed=91, kind="smallint", bias_mode="row")
+        C = ge.gemm2_epilogue(p1.A.cuda(), p1.B.t().contiguous().t().cuda(), p2.A.cuda(),
+                              p2.B.t().contiguous().t().cuda(), p1.bias.cuda(), tile_n=256, cta_group=2, multicast=2)
+        torch.cuda.synchronize()
+        out, _ = oracle.gemm2_epilogue(p1.A, p1.B, p2.A, p2.B, 1100, 700, 96, 160, bias=p1.bias, bias_mode="row")
+        assert np.array_equal(C.float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+        return
+    if variant == "long_k":
+        prob = workloads.make_problem(1024, 512, 64 * 37 + 5, seed=92, kind="smallint", bias_mode="row")
+        got = run_gpu(prob, "cr", tile_n=512, cta_group=2, multicast=2)
+        out, _ = oracle_run(prob, "cr")
+        assert np.array_equal(got, exact_expect(out, torch.float16))
+        return
+    bias_mode = "col" if variant == "f32_col" else "full"
+    dt = torch.float32 if variant == "f32_col" else torch.float16
+    prob = workloads.make_problem(900, 530, 150, seed=93, kind="smallint", bias_mode=bias_mode)
+    got = run_gpu(prob, "rc", out_dtype=dt, tile_n=512, cta_group=2, multicast=2)
+    out, _ = oracle_run(prob, "rc")
+    assert np.array_equal(got, exact_expect(out, dt))
+
+
+def test_multicast_rejects_prologue():
+    prob = workloads.make_problem(600, 512, 128, seed=94, kind="smallint", bias_mode="row", prologue="scale_k")
+    with pytest.raises(ge.GEError):
+        run_gpu(prob, "rr", multicast=2)
