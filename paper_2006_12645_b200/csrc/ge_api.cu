@@ -340,7 +340,7 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
         int splits = 0;
         // Split-K for few, long tiles, single-CTA tiles only: a cluster of S
         // CTAs per tile, one K-slice each, partials reduce-scattered over distributed shared
-        // memory ((S-1)/S of a 128 x BN fp32 tile sent per CTA at ~32 B/clk, plus the handshake).
+        // memory ((S-1)/S of a 128 x BN fp32 tile sent per CTA at ~9.5 B/clk, plus the handshake).
         // Co-resident clusters of S come from cudaOccupancyMaxActiveClusters (GPC-bound).
         if (cg == 1 && bn <= 256 && a.o.stream_k == 0 && nkb >= 8) {
             const int64_t smax = std::min<int64_t>(8, nkb / 4);
@@ -354,7 +354,10 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
                 int64_t conc_s = (cap && cap->cap[bi][S] > 0) ? cap->cap[bi][S]
                                                               : static_cast<int64_t>(kCap148[S] * (sms / 148.0));
                 conc_s = std::max<int64_t>(1, conc_s);
-                const double red = (S - 1.0) / S * 128.0 * bn * 4 / 32.0 + 2500.0;
+                // every CTA sends and receives (S-1)/S of its fp32 partial at once: ~9.5 B/clk each way
+                // measured (DSMEM is ~17 B/clk bidirectional; debug counters on 640x1024x3840,
+                // 2048x128x3456, 128x2176x3200: 8.6-10 B/clk effective)
+                const double red = (S - 1.0) / S * 128.0 * bn * 4 / 9.5 + 1500.0;
                 const double c_split = static_cast<double>(cdiv(tiles, conc_s)) *
                                        (static_cast<double>(cdiv(nkb, S)) * t_kb + red);
                 if (c_split < cost * (1 - 1e-9)) {
