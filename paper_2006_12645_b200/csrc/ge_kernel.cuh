@@ -904,20 +904,22 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
                 if constexpr (BATCH) {
+                    static_assert(CPH % 2 == 0, "paired drain");
+                    // chunks are drained two at a time (both TMEM loads in flight together), so the
+                    // half is released after CPH/2 - 1 chunk pairs of math instead of CPH - 1 chunks
                     uint32_t packed[CPH][NWORD];
 #pragma unroll
-                    for (int j = 0; j < CPH; ++j) {
-                        uint32_t v[W];
-                        const long long tl0 = (dbg && e_idx == 0) ? clock64() : 0;
-                        load(h * CPH_ALL + j * NG + grp, v);
-                        if (nkb > 0) ptx::tmem_ld_wait_regs(v);
-                        const long long tl1 = (dbg && e_idx == 0) ? clock64() : 0;
-                        if (j == CPH - 1) release(h);
-                        compute(h * CPH_ALL + j * NG + grp, v, packed[j]);
-                        if (dbg && e_idx == 0 && lane == 0) {
-                            dl[DBG_EPI_TMEMLD] += static_cast<unsigned long long>(tl1 - tl0);
-                            dl[DBG_EPI_MATH] += static_cast<unsigned long long>(clock64() - tl1);
+                    for (int j = 0; j < CPH; j += 2) {
+                        uint32_t va[W], vb[W];
+                        load(h * CPH_ALL + j * NG + grp, va);
+                        load(h * CPH_ALL + (j + 1) * NG + grp, vb);
+                        if (nkb > 0) {
+                            ptx::tmem_ld_wait_regs(va);
+                            ptx::tmem_ld_wait_regs(vb);
                         }
+                        if (j + 2 >= CPH) release(h);
+                        compute(h * CPH_ALL + j * NG + grp, va, packed[j]);
+                        compute(h * CPH_ALL + (j + 1) * NG + grp, vb, packed[j + 1]);
                     }
 #pragma unroll
                     for (int j = 0; j < CPH; ++j) store(h * CPH_ALL + j * NG + grp, packed[j]);
