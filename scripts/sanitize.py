@@ -15,5 +15,15 @@ for (M, N, K) in [(300, 520, 200), (129, 257, 65)]:
             ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, stream_k=sk)
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, prologue="scale_k", scale=scale, stream_k=1)
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, out_dtype=torch.float32, stream_k=1)
+        ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, op="literal_bias_relu", stream_k=1)
+    # multicast clusters of two CTA pairs (B tiles multicast to both pairs), both tile widths
+    for bn in (512, 256):
+        ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=2, multicast=2)
+        ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=2, multicast=2, out_dtype=torch.float32)
+    # split-K clusters (DSMEM reduce-scatter): a long-K shape the planner splits
+    A2 = torch.randn(256, 64 * 40, device="cuda", dtype=torch.float16)
+    B2 = torch.randn(64 * 40, 256, device="cuda", dtype=torch.float16)
+    b2 = torch.randn(256, device="cuda", dtype=torch.float16)
+    ge.gemm_epilogue(A2, B2, b2)
 torch.cuda.synchronize()
 print("sanitize workload done")
