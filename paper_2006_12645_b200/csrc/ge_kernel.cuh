@@ -45,6 +45,10 @@
 #ifndef GE_EPI_ONE_WAITER
 #define GE_EPI_ONE_WAITER 1
 #endif
+// Straight-line epilogue block for the measured configuration (ROW bias, ReLU); 0 = general code only.
+#ifndef GE_EPI_FAST
+#define GE_EPI_FAST 1
+#endif
 
 namespace ge {
 
@@ -573,6 +577,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         constexpr int NBUF = C_::kStagingBufs;
         uint8_t* stage_c = smem_c + e_idx * (NBUF * STG);
         const uint64_t pol_c = ptx::l2_policy(p.hint_c);
+        const bool epi_fast = C_::kBiasF32 && !p.literal && p.act == ACT_RELU && p.bias_mode == BIAS_ROW && !p.dbg_flags;
         int buf = 0;
         for (int jj = 0; jj < work.count(); ++jj) {
             const int it = work.epi_index(jj);
@@ -637,6 +642,33 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             };
             // S2 of Listing 1: v = acc + beta, relu, one RNE conversion; packed into NWORD words
             auto compute = [&](const int c, const uint32_t* v, uint32_t* w) {
+                if (GE_EPI_FAST && __builtin_expect(epi_fast, 1)) {
+                    // The measured configuration (ROW bias staged as pre-signed fp32, ReLU, one
+                    // rounding) as a short straight-line block: paired fp32 adds (FADD2, IEEE RN
+                    // like two FADDs), ReLU as max(v, +0) (-0 and NaN -> +0, R-C5), one RNE
+                    // pack per two outputs.  The last tile's drain is exposed on single-wave
+                    // shapes and was instruction-fetch bound with the general code inline.
+                    const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
+                    uint32_t r[W];
+#pragma unroll
+                    for (int g = 0; g < W / 4; ++g) {
+                        const float4 bf = bs[g];
+                        ptx::add_f32x2(v[4 * g], v[4 * g + 1], bf.x, bf.y, r[4 * g], r[4 * g + 1]);
+                        ptx::add_f32x2(v[4 * g + 2], v[4 * g + 3], bf.z, bf.w, r[4 * g + 2], r[4 * g + 3]);
+                    }
+                    if constexpr (OUT_F32) {
+#pragma unroll
+                        for (int e = 0; e < W; ++e) w[e] = __float_as_uint(fmaxf(__uint_as_float(r[e]), 0.0f));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < W / 2; ++e) {
+                            const __half2 hh = __floats2half2_rn(fmaxf(__uint_as_float(r[2 * e]), 0.0f),
+                                                                 fmaxf(__uint_as_float(r[2 * e + 1]), 0.0f));
+                            w[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                        }
+                    }
+                    return;
+                }
                 const int col0 = nt * BN + c * W;
                 const float bsg = p.bias_sign;
                 float f[W];

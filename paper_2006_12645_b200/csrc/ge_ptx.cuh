@@ -256,6 +256,17 @@ __device__ __forceinline__ void bulk_wait() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// (d0, d1) = (a0 + b0, a1 + b1): one paired fp32 add (FADD2), each lane IEEE round-to-nearest.
+__device__ __forceinline__ void add_f32x2(uint32_t a0, uint32_t a1, float b0, float b1, uint32_t& d0, uint32_t& d1) {
+    asm("{\n\t.reg .b64 x, y, z;\n\t"
+        "mov.b64 x, {%2, %3};\n\t"
+        "mov.b64 y, {%4, %5};\n\t"
+        "add.rn.f32x2 z, x, y;\n\t"
+        "mov.b64 {%0, %1}, z;\n\t}"
+        : "=r"(d0), "=r"(d1)
+        : "r"(a0), "r"(a1), "f"(b0), "f"(b1));
+}
+
 // Generic-proxy smem writes -> visible to the async proxy (TMA store, tcgen05.mma operands).
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
