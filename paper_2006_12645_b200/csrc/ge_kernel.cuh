@@ -46,6 +46,10 @@
 #define GE_EPI_ONE_WAITER 1
 #endif
 // Straight-line epilogue block for the measured configuration (ROW bias, ReLU); 0 = general code only.
+// End of the epilogue: wait for the TMA stores' smem reads only (1) or for their completion (0).
+#ifndef GE_END_WAIT_READ
+#define GE_END_WAIT_READ 0
+#endif
 #ifndef GE_EPI_FAST
 #define GE_EPI_FAST 1
 #endif
@@ -640,33 +644,36 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     else ptx::mbar_arrive(&tempty_bar[acc * NH + h]);
                 }
             };
+            // The measured configuration (ROW bias staged as pre-signed fp32, ReLU, one rounding) as
+            // a short straight-line block: paired fp32 adds (FADD2, IEEE RN like two FADDs), ReLU as
+            // max(v, +0) (-0 and NaN -> +0, R-C5), one RNE pack per two outputs.  The last tile's
+            // drain is exposed on single-wave shapes and was instruction-fetch bound (ncu: no_inst)
+            // with the general code inline, so it also gets its own chunk loop below.
+            auto compute_fast = [&](const int c, const uint32_t* v, uint32_t* w) {
+                const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
+                uint32_t r[W];
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g) {
+                    const float4 bf = bs[g];
+                    ptx::add_f32x2(v[4 * g], v[4 * g + 1], bf.x, bf.y, r[4 * g], r[4 * g + 1]);
+                    ptx::add_f32x2(v[4 * g + 2], v[4 * g + 3], bf.z, bf.w, r[4 * g + 2], r[4 * g + 3]);
+                }
+                if constexpr (OUT_F32) {
+#pragma unroll
+                    for (int e = 0; e < W; ++e) w[e] = __float_as_uint(fmaxf(__uint_as_float(r[e]), 0.0f));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < W / 2; ++e) {
+                        const __half2 hh = __floats2half2_rn(fmaxf(__uint_as_float(r[2 * e]), 0.0f),
+                                                             fmaxf(__uint_as_float(r[2 * e + 1]), 0.0f));
+                        w[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                    }
+                }
+            };
             // S2 of Listing 1: v = acc + beta, relu, one RNE conversion; packed into NWORD words
             auto compute = [&](const int c, const uint32_t* v, uint32_t* w) {
-                if (GE_EPI_FAST && __builtin_expect(epi_fast, 1)) {
-                    // The measured configuration (ROW bias staged as pre-signed fp32, ReLU, one
-                    // rounding) as a short straight-line block: paired fp32 adds (FADD2, IEEE RN
-                    // like two FADDs), ReLU as max(v, +0) (-0 and NaN -> +0, R-C5), one RNE
-                    // pack per two outputs.  The last tile's drain is exposed on single-wave
-                    // shapes and was instruction-fetch bound with the general code inline.
-                    const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
-                    uint32_t r[W];
-#pragma unroll
-                    for (int g = 0; g < W / 4; ++g) {
-                        const float4 bf = bs[g];
-                        ptx::add_f32x2(v[4 * g], v[4 * g + 1], bf.x, bf.y, r[4 * g], r[4 * g + 1]);
-                        ptx::add_f32x2(v[4 * g + 2], v[4 * g + 3], bf.z, bf.w, r[4 * g + 2], r[4 * g + 3]);
-                    }
-                    if constexpr (OUT_F32) {
-#pragma unroll
-                        for (int e = 0; e < W; ++e) w[e] = __float_as_uint(fmaxf(__uint_as_float(r[e]), 0.0f));
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < W / 2; ++e) {
-                            const __half2 hh = __floats2half2_rn(fmaxf(__uint_as_float(r[2 * e]), 0.0f),
-                                                                 fmaxf(__uint_as_float(r[2 * e + 1]), 0.0f));
-                            w[e] = *reinterpret_cast<const uint32_t*>(&hh);
-                        }
-                    }
+                if (GE_EPI_FAST && epi_fast) {
+                    compute_fast(c, v, w);
                     return;
                 }
                 const int col0 = nt * BN + c * W;
@@ -955,6 +962,18 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     }
 #pragma unroll
                     for (int j = 0; j < CPH; ++j) store(h * CPH_ALL + j * NG + grp, packed[j]);
+                } else if (GE_EPI_FAST && epi_fast && pc.kind != PIECE_OWNER && nkb > 0) {
+#pragma unroll 1
+                    for (int j = 0; j < CPH; ++j) {
+                        const int c = h * CPH_ALL + j * NG + grp;
+                        uint32_t v[W];
+                        ptx::tmem_ld_32x32b_x32(tm_row + c * W, v);
+                        ptx::tmem_ld_wait_regs(v);
+                        if (j == CPH - 1) release(h);
+                        uint32_t w[NWORD];
+                        compute_fast(c, v, w);
+                        store(c, w);
+                    }
                 } else {
 #pragma unroll 1
                     for (int j = 0; j < CPH; ++j) {
@@ -987,7 +1006,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             }
             if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
         }
-        if (p.c_tma && lane == 0) ptx::bulk_wait<0>();
+        // Only the staging reads must finish before the CTA exits: the stores' global writes
+        // complete with the grid (they are visible to the next kernel / PDL dependent and to the
+        // stream, as for any async-proxy write), so the exposed tail skips their write latency.
+        if (p.c_tma && lane == 0) {
+            if (GE_END_WAIT_READ) ptx::bulk_wait_read<0>();
+            else ptx::bulk_wait<0>();
+        }
         if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
     } else if (PRO && warp >= 4 + EPI_WARPS) {
         // ===================== prologue transform of the A stage (in place, in smem) ==========
