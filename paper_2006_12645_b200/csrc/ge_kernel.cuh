@@ -50,6 +50,10 @@
 #ifndef GE_END_WAIT_READ
 #define GE_END_WAIT_READ 0
 #endif
+// One dry iteration of the fast epilogue loop before the first accumulator wait (i-cache warm-up).
+#ifndef GE_EPI_WARM
+#define GE_EPI_WARM 0
+#endif
 #ifndef GE_EPI_FAST
 #define GE_EPI_FAST 1
 #endif
@@ -607,10 +611,15 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
                 ptx::named_bar_sync(1, EPI_WARPS * 32);
             }
-            if (nkb > 0) {
-                // One warp polls the accumulator barrier; the others sleep on a hardware named
-                // barrier (8 polling warps would contend with the MMA and TMA threads for the
-                // mbarrier unit during the whole mainloop).
+            // fast chunk loop of the first tile: one dry iteration before the accumulator wait
+            // (GE_EPI_WARM) pulls the loop's code into the instruction caches while the MMAs run
+            const bool fast_loop = GE_EPI_FAST && epi_fast && NH == 1 && !BATCH && pc.kind != PIECE_OWNER &&
+                                   pc.kind != PIECE_PARTIAL && pc.kind != PIECE_SPLIT && nkb > 0;
+            const bool warm = GE_EPI_WARM && fast_loop && jj == 0;
+            // One warp polls the accumulator barrier; the others sleep on a hardware named barrier
+            // (8 polling warps would contend with the MMA and TMA threads for the mbarrier unit
+            // during the whole mainloop).
+            auto wait_acc = [&]() {
                 if (GE_EPI_ONE_WAITER) {
                     if (e_idx == 0)
                         ptx::mbar_wait_timed(&tfull_bar[acc], acc_phase, dbg && lane == 0, dl[DBG_EPI_TFULL]);
@@ -619,7 +628,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     ptx::mbar_wait_timed(&tfull_bar[acc], acc_phase, dbg && e_idx == 0 && lane == 0, dl[DBG_EPI_TFULL]);
                 }
                 ptx::tc_fence_after();
-            }
+            };
+            if (nkb > 0 && !warm) wait_acc();
             const long long t_epi0 = (dbg && e_idx == 0) ? clock64() : 0;
             const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 
@@ -962,17 +972,24 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     }
 #pragma unroll
                     for (int j = 0; j < CPH; ++j) store(h * CPH_ALL + j * NG + grp, packed[j]);
-                } else if (GE_EPI_FAST && epi_fast && pc.kind != PIECE_OWNER && nkb > 0) {
+                } else if (fast_loop) {
 #pragma unroll 1
-                    for (int j = 0; j < CPH; ++j) {
-                        const int c = h * CPH_ALL + j * NG + grp;
+                    for (int j = warm ? -1 : 0; j < CPH; ++j) {
+                        const int c = h * CPH_ALL + (j < 0 ? 0 : j) * NG + grp;
                         uint32_t v[W];
-                        ptx::tmem_ld_32x32b_x32(tm_row + c * W, v);
-                        ptx::tmem_ld_wait_regs(v);
+                        if (j == 0 && warm) wait_acc();
+                        if (j >= 0) {
+                            ptx::tmem_ld_32x32b_x32(tm_row + c * W, v);
+                            ptx::tmem_ld_wait_regs(v);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < W; ++e) v[e] = 0u;
+                        }
                         if (j == CPH - 1) release(h);
                         uint32_t w[NWORD];
                         compute_fast(c, v, w);
-                        store(c, w);
+                        if (j >= 0) store(c, w);
+                        else if (w[0] == 0xFFFFFFFFu) __nanosleep(0);   // keep the dry iteration's math
                     }
                 } else {
 #pragma unroll 1

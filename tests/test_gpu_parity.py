@@ -547,3 +547,32 @@ def test_multicast_rejects_prologue():
     prob = workloads.make_problem(600, 512, 128, seed=94, kind="smallint", bias_mode="row", prologue="scale_k")
     with pytest.raises(ge.GEError):
         run_gpu(prob, "rr", multicast=2)
+
+
+@pytest.mark.parametrize("tile_n,cg", CONFIGS)
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.float32])
+@pytest.mark.parametrize("N", [1096, 1100])       # TMA store / st.global fallback (row pitch not 16-B aligned)
+def test_fast_epilogue_matches_general(tile_n, cg, out_dtype, N):
+    """The straight-line epilogue of the measured configuration (ROW bias + ReLU: FADD2, max(v,+0),
+    one RNE pack) against the general epilogue code on the same accumulators: FULL bias holding
+    the row bias broadcast to every row takes the general path and must agree bitwise (same fp32
+    add, same ReLU, same rounding; DESIGN.md R-C5/R-C6).  Uniform data (no exactness needed: both
+    read one accumulator), several 32-column chunks per warp, a ragged tail, zero rows in A (ReLU
+    of +-0 bias: no -0 may reach C), and the bound against the oracle."""
+    prob = workloads.make_problem(300, N, 320, seed=71, kind="uniform", bias_mode="row")
+    prob.A[:7] = 0.0
+    prob.bias[::5] = -0.0
+    A, B = dev_operands(prob, "rc")
+    bias = prob.bias.cuda()
+    fast = ge.gemm_epilogue(A, B, bias, op="bias_relu", bias_mode="row", out_dtype=out_dtype,
+                            tile_n=tile_n, cta_group=cg)
+    full = bias.view(1, -1).expand(prob.M, -1).contiguous()
+    gen = ge.gemm_epilogue(A, B, full, op="bias_relu", bias_mode="full", out_dtype=out_dtype,
+                           tile_n=tile_n, cta_group=cg)
+    torch.cuda.synchronize()
+    bits = torch.int16 if out_dtype == torch.float16 else torch.int32
+    assert torch.equal(fast.view(bits), gen.view(bits))
+    assert not bool(torch.signbit(fast).any())
+    got = fast.float().cpu().numpy().astype(np.float64)
+    out, mag = oracle_run(prob, "rc")
+    check_bound(got, out, mag, "fast epilogue")
