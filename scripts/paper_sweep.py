@@ -21,13 +21,16 @@ import torch
 import paper_2006_12645_b200 as ge
 
 
-def timed(fn_per_set, nsets, it=20):
+def timed(fn_per_set, nsets, it=20, cpg=1):
+    """Seconds per call.  cpg = calls captured per graph (operand sets rotating inside the graph):
+    1 includes the per-graph launch gap in every call; larger values amortise it (kernel throughput)."""
     graphs = []
-    for i in range(nsets):
+    for i in range(nsets if cpg == 1 else 1):
         fn_per_set(i)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn_per_set(i)
+            for r in range(cpg):
+                fn_per_set((i + r) % nsets)
         graphs.append(g)
     for g in graphs[:2]:
         g.replay()
@@ -35,10 +38,10 @@ def timed(fn_per_set, nsets, it=20):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for i in range(it):
-        graphs[i % nsets].replay()
+        graphs[i % len(graphs)].replay()
     e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / it * 1e-3
+    return s.elapsed_time(e) / (it * cpg) * 1e-3
 
 
 def main():
@@ -46,6 +49,7 @@ def main():
     ap.add_argument("--n", type=int, default=100)
     ap.add_argument("--seed", type=int, default=2006)
     ap.add_argument("--out", default="gpurun_out/paper_sweep.json")
+    ap.add_argument("--cpg", type=int, default=1, help="calls per CUDA graph (1: one graph launch per call)")
     a = ap.parse_args()
     rng = random.Random(a.seed)
     shapes = [tuple(128 * rng.randint(1, 32) for _ in range(3)) for _ in range(a.n)]
@@ -56,9 +60,9 @@ def main():
                  torch.randn(N, K, device="cuda", dtype=torch.float16).t() * 0.5) for _ in range(nsets)]
         bias = torch.randn(N, device="cuda", dtype=torch.float16)
         C = torch.empty(M, N, device="cuda", dtype=torch.float16)
-        t_ours = timed(lambda i: ge.gemm_epilogue(sets[i][0], sets[i][1], bias, out=C), nsets)
-        t_unf = timed(lambda i: torch.relu_(torch.matmul(sets[i][0], sets[i][1]).add_(bias)), nsets)
-        t_lt = timed(lambda i: torch._addmm_activation(bias, sets[i][0], sets[i][1]), nsets)
+        t_ours = timed(lambda i: ge.gemm_epilogue(sets[i][0], sets[i][1], bias, out=C), nsets, cpg=a.cpg)
+        t_unf = timed(lambda i: torch.relu_(torch.matmul(sets[i][0], sets[i][1]).add_(bias)), nsets, cpg=a.cpg)
+        t_lt = timed(lambda i: torch._addmm_activation(bias, sets[i][0], sets[i][1]), nsets, cpg=a.cpg)
         fl = 2.0 * M * N * K
         rows.append({"M": M, "N": N, "K": K, "ours_tflops": fl / t_ours / 1e12, "unfused_tflops": fl / t_unf / 1e12,
                      "cublaslt_tflops": fl / t_lt / 1e12, "speedup_vs_unfused": t_unf / t_ours,
@@ -70,7 +74,7 @@ def main():
         return {"faster_count": sum(x > 1.0 for x in v), "n": len(v), "peak": max(v), "worst": min(v),
                 "geomean": math.exp(sum(math.log(x) for x in v) / len(v)), "mean": sum(v) / len(v)}
     out = {"experiment": "paper-shaped random sweep (PAPER.md Fig. 17 analog): GEMM+bias+ReLU, rc layout",
-           "seed": a.seed, "vs_unfused": summary("speedup_vs_unfused"), "vs_cublaslt": summary("speedup_vs_cublaslt"),
+           "seed": a.seed, "calls_per_graph": a.cpg, "vs_unfused": summary("speedup_vs_unfused"), "vs_cublaslt": summary("speedup_vs_cublaslt"),
            "paper_gv100_vs_cublas_cudnn": {"faster_count": 94, "n": 100, "peak": 2.55, "worst": 0.89, "mean": 1.29,
                                            "source": "PAPER.md:1327-1330 (other hardware, context only)"},
            "rows": rows}
