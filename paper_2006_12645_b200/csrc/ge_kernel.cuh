@@ -54,6 +54,10 @@
 #ifndef GE_EPI_WARM
 #define GE_EPI_WARM 0
 #endif
+// The fast epilogue also for the 512-wide pair tile (fp16 bias slice).
+#ifndef GE_EPI_FAST512
+#define GE_EPI_FAST512 1
+#endif
 #ifndef GE_EPI_FAST
 #define GE_EPI_FAST 1
 #endif
@@ -585,7 +589,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         constexpr int NBUF = C_::kStagingBufs;
         uint8_t* stage_c = smem_c + e_idx * (NBUF * STG);
         const uint64_t pol_c = ptx::l2_policy(p.hint_c);
-        const bool epi_fast = C_::kBiasF32 && !p.literal && p.act == ACT_RELU && p.bias_mode == BIAS_ROW && !p.dbg_flags;
+        const bool epi_fast = (C_::kBiasF32 || (GE_EPI_FAST512 && p.bias_sign > 0.0f)) && !p.literal && p.act == ACT_RELU &&
+                              p.bias_mode == BIAS_ROW && !p.dbg_flags;
         int buf = 0;
         for (int jj = 0; jj < work.count(); ++jj) {
             const int it = work.epi_index(jj);
@@ -660,13 +665,29 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // drain is exposed on single-wave shapes and was instruction-fetch bound (ncu: no_inst)
             // with the general code inline, so it also gets its own chunk loop below.
             auto compute_fast = [&](const int c, const uint32_t* v, uint32_t* w) {
-                const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
                 uint32_t r[W];
+                if constexpr (C_::kBiasF32) {
+                    const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
 #pragma unroll
-                for (int g = 0; g < W / 4; ++g) {
-                    const float4 bf = bs[g];
-                    ptx::add_f32x2(v[4 * g], v[4 * g + 1], bf.x, bf.y, r[4 * g], r[4 * g + 1]);
-                    ptx::add_f32x2(v[4 * g + 2], v[4 * g + 3], bf.z, bf.w, r[4 * g + 2], r[4 * g + 3]);
+                    for (int g = 0; g < W / 4; ++g) {
+                        const float4 bf = bs[g];
+                        ptx::add_f32x2(v[4 * g], v[4 * g + 1], bf.x, bf.y, r[4 * g], r[4 * g + 1]);
+                        ptx::add_f32x2(v[4 * g + 2], v[4 * g + 3], bf.z, bf.w, r[4 * g + 2], r[4 * g + 3]);
+                    }
+                } else {
+                    // 512-wide tiles stage the slice as fp16 (no smem left for fp32); added bias only
+                    const uint4* bs = reinterpret_cast<const uint4*>(smem_bias + c * W);       // broadcast reads
+#pragma unroll
+                    for (int g = 0; g < W / 8; ++g) {
+                        const uint4 hb = bs[g];
+                        const __half2* h2 = reinterpret_cast<const __half2*>(&hb);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 bf = __half22float2(h2[e]);
+                            ptx::add_f32x2(v[8 * g + 2 * e], v[8 * g + 2 * e + 1], bf.x, bf.y, r[8 * g + 2 * e],
+                                           r[8 * g + 2 * e + 1]);
+                        }
+                    }
                 }
                 if constexpr (OUT_F32) {
 #pragma unroll
