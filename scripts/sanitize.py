@@ -10,7 +10,7 @@ for (M, N, K) in [(300, 520, 200), (129, 257, 65)]:
     B = torch.randn(N, up8(K), device="cuda", dtype=torch.float16)[:, :K].t()
     bias = torch.randn(N, device="cuda", dtype=torch.float16)
     scale = torch.rand(K, device="cuda") + 0.5
-    for bn, cg in [(512, 2), (256, 2), (256, 1), (128, 2), (128, 1), (64, 1)]:
+    for bn, cg in [(512, 2), (256, 2), (192, 2), (256, 1), (192, 1), (128, 2), (128, 1), (64, 1)]:
         for sk in (1, 2):
             ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, stream_k=sk)
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=cg, prologue="scale_k", scale=scale, stream_k=1)
