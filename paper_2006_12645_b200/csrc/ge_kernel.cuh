@@ -50,9 +50,9 @@
 #ifndef GE_END_WAIT_READ
 #define GE_END_WAIT_READ 0
 #endif
-// One dry iteration of the fast epilogue loop before the first accumulator wait (i-cache warm-up).
-#ifndef GE_EPI_WARM
-#define GE_EPI_WARM 0
+// Fast epilogue loop drains two TMEM chunks per iteration (both loads in flight together).
+#ifndef GE_EPI_PAIRLD
+#define GE_EPI_PAIRLD 0
 #endif
 // The fast epilogue also for the 512-wide pair tile (fp16 bias slice).
 #ifndef GE_EPI_FAST512
@@ -616,11 +616,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
                 ptx::named_bar_sync(1, EPI_WARPS * 32);
             }
-            // fast chunk loop of the first tile: one dry iteration before the accumulator wait
-            // (GE_EPI_WARM) pulls the loop's code into the instruction caches while the MMAs run
+            // straight-line chunk loop of the measured configuration (see compute_fast)
             const bool fast_loop = GE_EPI_FAST && epi_fast && NH == 1 && !BATCH && pc.kind != PIECE_OWNER &&
                                    pc.kind != PIECE_PARTIAL && pc.kind != PIECE_SPLIT && nkb > 0;
-            const bool warm = GE_EPI_WARM && fast_loop && jj == 0;
             // One warp polls the accumulator barrier; the others sleep on a hardware named barrier
             // (8 polling warps would contend with the MMA and TMA threads for the mbarrier unit
             // during the whole mainloop).
@@ -634,7 +632,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
                 ptx::tc_fence_after();
             };
-            if (nkb > 0 && !warm) wait_acc();
+            if (nkb > 0) wait_acc();
             const long long t_epi0 = (dbg && e_idx == 0) ? clock64() : 0;
             const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 
@@ -994,23 +992,36 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
                     for (int j = 0; j < CPH; ++j) store(h * CPH_ALL + j * NG + grp, packed[j]);
                 } else if (fast_loop) {
+                    if constexpr (GE_EPI_PAIRLD && CPH % 2 == 0) {
+                        // two chunks' TMEM loads in flight together (the last tile's drain is
+                        // exposed on single-wave shapes)
 #pragma unroll 1
-                    for (int j = warm ? -1 : 0; j < CPH; ++j) {
-                        const int c = h * CPH_ALL + (j < 0 ? 0 : j) * NG + grp;
-                        uint32_t v[W];
-                        if (j == 0 && warm) wait_acc();
-                        if (j >= 0) {
+                        for (int j = 0; j < CPH; j += 2) {
+                            const int c0 = h * CPH_ALL + j * NG + grp, c1 = c0 + NG;
+                            uint32_t va[W], vb[W];
+                            ptx::tmem_ld_32x32b_x32(tm_row + c0 * W, va);
+                            ptx::tmem_ld_32x32b_x32(tm_row + c1 * W, vb);
+                            ptx::tmem_ld_wait_regs(va);
+                            ptx::tmem_ld_wait_regs(vb);
+                            if (j + 2 >= CPH) release(h);
+                            uint32_t w[NWORD];
+                            compute_fast(c0, va, w);
+                            store(c0, w);
+                            compute_fast(c1, vb, w);
+                            store(c1, w);
+                        }
+                    } else {
+#pragma unroll 1
+                        for (int j = 0; j < CPH; ++j) {
+                            const int c = h * CPH_ALL + j * NG + grp;
+                            uint32_t v[W];
                             ptx::tmem_ld_32x32b_x32(tm_row + c * W, v);
                             ptx::tmem_ld_wait_regs(v);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < W; ++e) v[e] = 0u;
+                            if (j == CPH - 1) release(h);
+                            uint32_t w[NWORD];
+                            compute_fast(c, v, w);
+                            store(c, w);
                         }
-                        if (j == CPH - 1) release(h);
-                        uint32_t w[NWORD];
-                        compute_fast(c, v, w);
-                        if (j >= 0) store(c, w);
-                        else if (w[0] == 0xFFFFFFFFu) __nanosleep(0);   // keep the dry iteration's math
                     }
                 } else {
 #pragma unroll 1
