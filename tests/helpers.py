@@ -46,3 +46,21 @@ def check_bound(got: np.ndarray, out: np.ndarray, mag: np.ndarray, what: str = "
 
 def f16_bits(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+def check_relu_invariant(got: np.ndarray, pre: np.ndarray, mag: np.ndarray, what: str = ""):
+    """BASELINE.json north_star ReLU invariant on the GPU output, given the oracle's unrounded
+    pre-activation: every value is >= 0, finite and not -0 (DESIGN.md R-C5); it is exactly +0
+    wherever pre <= -tol, and > 0 wherever pre >= tol and RNE_fp16(pre) > 0 (tol = the per-element
+    bound; the band |pre| < tol is where rounding may legitimately decide the sign).
+    Returns (#forced zeros, #forced positives) so callers can assert both branches were exercised."""
+    got = np.asarray(got, dtype=np.float64)
+    tol = oracle.bound(pre, mag) + 2.0 ** -25
+    assert np.isfinite(got).all(), f"{what}: non-finite output"
+    assert (got >= 0).all(), f"{what}: negative output after ReLU"
+    assert not np.signbit(got).any(), f"{what}: -0 in the output (ReLU must give +0)"
+    neg = pre <= -tol
+    assert (got[neg] == 0).all(), f"{what}: {int((got[neg] != 0).sum())} nonzero outputs where pre <= -tol"
+    pos = (pre >= tol) & (oracle.f16_decode(oracle.f16_encode(pre)) > 0)
+    assert (got[pos] > 0).all(), f"{what}: {int((got[pos] <= 0).sum())} zero outputs where pre >= tol"
+    return int(neg.sum()), int(pos.sum())

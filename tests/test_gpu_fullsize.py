@@ -1,8 +1,11 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py uses (the
-default tile heuristic), checked against the oracle on sampled outputs: every element of the tile
-boundary rows/columns {0, 127, 128, 255, 256, last} plus seeded random rows x columns (the oracle
-evaluates the cross product of the sampled rows and columns).  Uniform data is held to the
-north_star bound; small-integer data (exact in fp32 in any order) bitwise."""
+default tile heuristic).  Up to 4096^3 (<= 2^36 FMA) the WHOLE output matrix is
+compared with the oracle in every layout; above that (8192^3, the batch) the check is sampled:
+every element of the tile-boundary rows/columns {0, 127, 128, 255, 256, 511, 512, 1023, 1024,
+last} (the 128-row CTA tile, the 256-row pair tile, the 512-column pair tile and their
+neighbours) plus seeded random rows x columns (the oracle evaluates the cross product of the
+sampled rows and columns).  Uniform data is held to the north_star bound and the ReLU invariant;
+small-integer data (exact in fp32 in any order) bitwise."""
 from __future__ import annotations
 
 import functools
@@ -13,7 +16,7 @@ import torch
 
 import oracle
 import workloads
-from tests.helpers import check_bound, oracle_run
+from tests.helpers import check_bound, check_relu_invariant, oracle_run
 
 pytestmark = pytest.mark.gpu
 ge = pytest.importorskip("paper_2006_12645_b200")
@@ -21,7 +24,7 @@ ge = pytest.importorskip("paper_2006_12645_b200")
 
 def sample_idx(n, k, seed):
     g = np.random.default_rng(seed)
-    base = [i for i in (0, 127, 128, 255, 256, n - 1) if 0 <= i < n]
+    base = [i for i in (0, 127, 128, 255, 256, 511, 512, 1023, 1024, n - 1) if 0 <= i < n]
     extra = g.choice(n, size=min(k, n), replace=False)
     return np.unique(np.concatenate([base, extra])).astype(np.int64)
 
@@ -61,11 +64,13 @@ def check(prob, layouts, kind, nsamp=160, **kw):
     rows = sample_idx(prob.M, nsamp, 1)
     cols = sample_idx(prob.N, nsamp, 2)
     got = run_sampled(prob, layouts, rows, cols, **kw)
-    out, mag = oracle_run(prob, layouts, rows=rows, cols=cols)
+    pre, mag = oracle_run(prob, layouts, rows=rows, cols=cols, relu=False)
+    out = np.where(pre > 0, pre, 0.0)          # relu(pre), pinned by test_relu_invariant (CPU)
     if kind == "smallint":
         assert np.array_equal(got, oracle.f16_decode(oracle.f16_encode(out))), layouts
     else:
         check_bound(got, out, mag, layouts)
+        check_relu_invariant(got, pre, mag, layouts)
 
 
 @pytest.mark.parametrize("kind", ["uniform", "smallint"])
@@ -75,10 +80,43 @@ def test_square_8192(layouts, kind):
     check(problem(8192, 8192, 8192, 51, kind), layouts, kind)
 
 
-@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
-def test_square_sweep_smaller(layouts):
-    for n in (1024, 2048, 4096):
-        check(problem(n, n, n, 52, "uniform"), layouts, "uniform", nsamp=96)
+@functools.lru_cache(maxsize=1)
+def full_oracle(n, seed, kind):
+    """Full n x n oracle (pre-activation, mag) of the rr problem; the oracle is layout invariant
+    bitwise (pinned on the CPU by test_layout_invariance_bitwise), so one evaluation serves all four
+    layouts of the same logical operands."""
+    return oracle_run(problem(n, n, n, seed, kind), "rr", relu=False)
+
+
+def run_full(prob, layouts):
+    A, B = to_dev(prob, layouts)
+    C = torch.empty((prob.M, prob.N), dtype=torch.float16, device="cuda")
+    ge.gemm_epilogue(A, B, prob.bias.cuda(), out=C)
+    torch.cuda.synchronize()
+    return C.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+def test_square_full_matrix(n):
+    """BASELINE configs[1] at 1024^3 / 2048^3 / 4096^3, all four layouts, EVERY output element against
+    the oracle (north_star bound + ReLU invariant), in the bench's launch configuration."""
+    prob = problem(n, n, n, 52, "uniform")
+    pre, mag = full_oracle(n, 52, "uniform")
+    out = np.where(pre > 0, pre, 0.0)
+    for layouts in workloads.LAYOUTS:
+        got = run_full(prob, layouts)
+        check_bound(got, out, mag, f"{n}^3 {layouts}")
+        nz, npos = check_relu_invariant(got, pre, mag, f"{n}^3 {layouts}")
+        assert nz > n * n // 4 and npos > n * n // 4
+
+
+def test_square_full_matrix_smallint_2048():
+    """2048^3 small-integer data, all four layouts, the whole matrix bitwise equal to RNE(oracle)."""
+    prob = problem(2048, 2048, 2048, 57, "smallint")
+    pre, _ = full_oracle(2048, 57, "smallint")
+    want = oracle.f16_decode(oracle.f16_encode(np.where(pre > 0, pre, 0.0)))
+    for layouts in workloads.LAYOUTS:
+        assert np.array_equal(run_full(prob, layouts), want), layouts
 
 
 @pytest.mark.parametrize("kind", ["uniform", "smallint"])

@@ -12,7 +12,10 @@ import torch
 
 import oracle
 import workloads
-from tests.helpers import check_bound, oracle_run
+import json
+import os
+
+from tests.helpers import check_bound, check_relu_invariant, oracle_run
 
 pytestmark = pytest.mark.gpu
 
@@ -55,11 +58,64 @@ def test_layouts_ragged(layouts, kind):
     """All four layouts on a ragged 300x520x200 problem spanning several tiles."""
     prob = workloads.make_problem(300, 520, 200, seed=31, kind=kind, bias_mode="row")
     got = run_gpu(prob, layouts)
-    out, mag = oracle_run(prob, layouts)
+    pre, mag = oracle_run(prob, layouts, relu=False)
+    out = np.where(pre > 0, pre, 0.0)          # relu(pre), pinned by test_relu_invariant (CPU)
     if kind == "smallint":
         assert np.array_equal(got, exact_expect(out, torch.float16))
     else:
         check_bound(got, out, mag, layouts)
+        check_relu_invariant(got, pre, mag, layouts)
+
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "hand_cases.json")
+
+
+def _golden():
+    with open(GOLDEN) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", _golden(), ids=lambda c: c["name"])
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_golden_cases_on_gpu(case, layouts):
+    """The hand-computed cases of tests/golden/hand_cases.json (each citing its passage: Listing 1,
+    Listing 5, the bias modes, the paper-literal rounding point R-C3, K = 0) through the CUDA path:
+    every golden value is exactly computable in fp32, so the GPU must return RNE_fp16(golden)
+    bitwise (fp16 out) and the golden value itself (fp32 out)."""
+    M, N, K = case["M"], case["N"], case["K"]
+    if K == 0 and layouts != "rr":
+        pytest.skip("K = 0 is covered in rr (no operand is read)")
+    A = torch.tensor(case["A"], dtype=torch.float16).reshape(M, K)
+    B = torch.tensor(case["B"], dtype=torch.float16).reshape(K, N)
+    bias = None if case["bias"] is None else torch.tensor(case["bias"], dtype=torch.float16)
+    scale = None if case.get("scale") is None else torch.tensor(case["scale"], dtype=torch.float32)
+    prob = workloads.Problem(M, N, K, A, B, bias, scale, {"bias_mode": case["bias_mode"], "prologue": case["prologue"]})
+    op = ("bias_" if bias is not None else "") + ("relu" if case["relu"] else "")
+    op = {"bias_": "bias", "": "none"}.get(op, op)
+    if case.get("literal_round"):
+        op = "literal_" + op
+    want = np.array(case["out"], dtype=np.float64).reshape(M, N)
+    for dt in (torch.float16, torch.float32):
+        got = run_gpu(prob, layouts, op=op, out_dtype=dt)
+        # fp32 out of the literal reading is the fp16-rounded pre-activation (exact in fp32)
+        assert np.array_equal(got, exact_expect(want, dt)), (case["name"], layouts, dt, got, want)
+        if case["relu"]:
+            assert not np.signbit(got).any()
+
+
+@pytest.mark.parametrize("tile_n,cg", CONFIGS)
+@pytest.mark.parametrize("layouts", ["rc", "cr"])
+def test_relu_invariant_uniform(tile_n, cg, layouts):
+    """BASELINE.json north_star ReLU invariant on the GPU output for uniform data, every kernel
+    configuration: C >= 0, no -0, exactly +0 where pre <= -tol and > 0 where pre >= tol."""
+    if (tile_n, cg) == (192, 2) and layouts[1] == "r":
+        pytest.skip("the 256 x 192 pair tile needs a K-major B")
+    prob = workloads.make_problem(333, 777, 321, seed=30, kind="uniform", bias_mode="row")
+    got = run_gpu(prob, layouts, tile_n=tile_n, cta_group=cg)
+    pre, mag = oracle_run(prob, layouts, relu=False)
+    nz, npos = check_relu_invariant(got, pre, mag, f"{tile_n}x{cg} {layouts}")
+    assert nz > 1000 and npos > 1000
+    check_bound(got, np.where(pre > 0, pre, 0.0), mag, "relu")
 
 
 @pytest.mark.parametrize("tile_n,cg", CONFIGS)

@@ -76,10 +76,35 @@ def test_hand_computed_cases(case, layouts):
     scale = None if case.get("scale") is None else torch.tensor(case["scale"], dtype=torch.float32)
     prob = workloads.Problem(M, N, K, A, B, bias, scale,
                              {"bias_mode": case["bias_mode"], "prologue": case["prologue"]})
-    out, mag = oracle_run(prob, layouts, relu=case["relu"])
+    out, mag = oracle_run(prob, layouts, relu=case["relu"], literal_round=case.get("literal_round", False))
     assert np.array_equal(out, np.array(case["out"], dtype=np.float64).reshape(M, N))
     assert np.array_equal(mag, np.array(case["mag"], dtype=np.float64).reshape(M, N))
     assert not np.signbit(out[out == 0]).any() or not case["relu"]
+
+
+def test_literal_golden_cases_reject_wrong_rounding_points():
+    """Negative controls for the literal-rounding pins (DESIGN.md R-C3): on the
+    hand-computed literal cases, an evaluation that rounds once (f16(acc + beta)), or that skips
+    either of the two roundings, must disagree with the golden value in at least one case each."""
+    lit = [c for c in _golden_cases() if c.get("literal_round")]
+    assert len(lit) >= 4
+    f16 = lambda x: oracle.f16_decode(oracle.f16_encode(np.asarray(x, dtype=np.float64)))
+    miss = {"single (no first rounding)": 0, "no second rounding": 0, "no rounding": 0}
+    for c in lit:
+        M, N, K = c["M"], c["N"], c["K"]
+        A = np.array(c["A"], dtype=np.float64).reshape(M, K)
+        B = np.array(c["B"], dtype=np.float64).reshape(K, N)
+        acc = A @ B                                  # exact: small integers and powers of two
+        b = np.array(c["bias"], dtype=np.float64)
+        beta = b[None, :] if c["bias_mode"] == "row" else b[:, None]
+        relu = (lambda v: np.where(v > 0, v, 0.0)) if c["relu"] else (lambda v: v)
+        want = np.array(c["out"], dtype=np.float64).reshape(M, N)
+        miss["single (no first rounding)"] += not np.array_equal(relu(f16(acc + beta)), want)
+        miss["no second rounding"] += not np.array_equal(relu(f16(acc) + beta), want)
+        miss["no rounding"] += not np.array_equal(relu(acc + beta), want)
+        # and the golden value is what the two-rounding definition gives (consistency of the file)
+        assert np.array_equal(relu(f16(f16(acc) + beta)), want), c["name"]
+    assert all(v >= 1 for v in miss.values()), miss
 
 
 # ---------------------------------------------------------------- brute force, exact rationals
