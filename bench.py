@@ -4,10 +4,14 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
 
 A "step" is one pass of the whole hot path over one batch of
-synthetic input.  Default workload (BASELINE.json configs[1], the configuration the metric is
-quoted on, at its largest size): M = N = K = 8192, bias (row) + ReLU, fp16 out, in all four
-operand layouts rr/rc/cr/cc -> 4 fused launches per step.  Each rank runs its own independent
-problem (seeded by rank): no collective on the data path, weak scaling.
+synthetic input.  Default workload at N = 1 (BASELINE.json configs[1], the configuration the
+metric is quoted on, at its largest size): M = N = K = 8192, bias (row) + ReLU, fp16 out, in all
+four operand layouts rr/rc/cr/cc -> 4 fused launches per step.  Default at N > 1 (north_star:
+"scaling ... to 8 GPUs on sharded batches", BASELINE.json configs[4]): batched64x2048, a GLOBAL
+batch of 64 items of 2048^3 sharded by batch with sharded.sharded_gemm_epilogue_batched (rank r
+owns items [r*64/N, (r+1)*64/N), generated from per-item seeds so shards do not depend on N), no
+collective on the data path, strong scaling; the N = 1 line carries that workload's N = 1 point
+as "scale_series" so the series is comparable.
 
 Timing: W untimed warm-up steps; K timed steps bracketed by barrier + synchronize, CUDA events
 on the launching stream, max over ranks.  Operands (256 MiB per layout per step) exceed the
@@ -34,7 +38,8 @@ METRIC = "TFLOP/s fused GEMM+bias+ReLU (fp16 in, fp32 acc) and % of B200 tensor 
 UNIT = "TFLOP/s"
 
 WORKLOADS = {
-    # name: (batch, M, N, K, layouts, prologue)
+    # name: (batch, M, N, K, layouts, prologue); batched64x2048's batch is GLOBAL (sharded over ranks)
+    "square256": (1, 256, 256, 256, ("rr",), None),
     "square8192": (1, 8192, 8192, 8192, ("rr", "rc", "cr", "cc"), None),
     "square4096": (1, 4096, 4096, 4096, ("rr", "rc", "cr", "cc"), None),
     "square2048": (1, 2048, 2048, 2048, ("rr", "rc", "cr", "cc"), None),
@@ -51,7 +56,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="square8192", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="auto", choices=["auto"] + sorted(WORKLOADS),
+                    help="auto: square8192 at N = 1, batched64x2048 (global batch sharded) at N > 1")
+    ap.add_argument("--gather", action="store_true", help="batched64x2048 at N > 1: also time the optional "
+                    "NCCL all-gather of the output shards (reported separately, off the hot path)")
+    ap.add_argument("--no-scale-series", action="store_true")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -68,13 +77,29 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(name, world):
+SHARDED = ("batched64x2048",)       # global batch sharded over ranks (strong scaling)
+
+
+def resolve_workload(name, world):
+    if name == "auto":
+        return "square8192" if world == 1 else "batched64x2048"
+    return name
+
+
+def workload_config(name, world, rank=0):
     batch, M, N, K, layouts, pro = WORKLOADS[name]
     cfg = {"workload": f"{name}: M=N=K={M}" if M == N == K else f"{name}: M={M} N={N} K={K}",
            "M": M, "N": N, "K": K, "batch_per_gpu": batch, "layouts": list(layouts),
            "epilogue": "bias_relu", "bias": "row (length N)", "prologue": pro or "none", "out": "f16",
            "global_batch": batch * len(layouts) * world,
            "parallelism": f"dp{world} (independent problem per GPU, no collective)"}
+    if name in SHARDED:
+        from paper_2006_12645_b200 import sharded
+        lo, hi = sharded.shard_range(batch, rank, world)
+        cfg.update({"batch_per_gpu": hi - lo, "global_batch": batch,
+                    "bias": "row, one per item (length N)",
+                    "parallelism": f"dp{world}: global batch {batch} sharded by batch (sharded_gemm_epilogue_batched, "
+                                   f"rank r owns items [r*{batch}/{world}, (r+1)*{batch}/{world})), no collective"})
     return cfg
 
 
@@ -160,8 +185,9 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    batch, M, N, K, layouts, pro = WORKLOADS[args.workload]
-    cfg = workload_config(args.workload, 1)
+    name = resolve_workload(args.workload, world)
+    batch, M, N, K, layouts, pro = WORKLOADS[name]
+    cfg = workload_config(name, world, 0)
     # each step: one bounded sample, sized so warmup+steps fit in ~120 s
     per_step = max(0.05, 120.0 / max(1, args.steps + args.warmup))
     rate, cores, desc, t = oracle_rate(M, N, K, seed=0, budget_s=per_step)
@@ -187,13 +213,16 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-def measured_peak():
+def measured_peaks():
+    """(bf16 burst TF/s, sustained TF/s, HBM GB/s, source) from the driver-written MEASURED_PEAKS.json,
+    else the B200_PROFILING.md fallbacks."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         mp = json.load(open(p))
-        return float(mp["bf16_tflops"]), float(mp.get("bf16_tflops_sustained", 0)) or None, "measured"
+        return (float(mp["bf16_tflops"]), float(mp.get("bf16_tflops_sustained", 0)) or None, float(mp["hbm_gbs"]),
+                "measured")
     except Exception:
-        return 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+        return 1590.0, 1400.0, 6500.0, "fallback (B200_PROFILING.md)"
 
 
 def ncu_traffic(workload):
@@ -208,12 +237,159 @@ def ncu_traffic(workload):
         return None, None
 
 
+def algorithmic_bytes(batch, M, N, K, pro):
+    """What one launch must move: A, B, C (fp16) per item, the ROW bias per item
+    (bench uses one per item for batches, one shared otherwise) and the SCALE_K vector."""
+    per_item = 2 * M * K + 2 * K * N + 2 * M * N
+    bias = 2 * N * (batch if batch > 1 else 1)
+    return batch * per_item + bias + (4 * K if pro == "scale_k" else 0)
+
+
+class Workload:
+    """Synthetic operands of one bench workload on this rank, the fused launch of one step, and
+    CUDA graphs of the step.  Operand sets rotate between steps so the working set exceeds the
+    126 MB L2 (no flush kernel in the timed region)."""
+
+    def __init__(self, name, dev, rank, world, torch, ge):
+        self.name, self.torch, self.ge = name, torch, ge
+        gbatch, M, N, K, layouts, pro = WORKLOADS[name]
+        self.M, self.N, self.K, self.layouts, self.pro = M, N, K, layouts, pro
+        self.sharded = name in SHARDED
+        if self.sharded:
+            from paper_2006_12645_b200 import sharded
+            self.lo, self.hi = sharded.shard_range(gbatch, rank, world)
+            self.batch, self.gbatch = self.hi - self.lo, gbatch
+        else:
+            self.lo, self.hi, self.batch, self.gbatch = 0, gbatch, gbatch, gbatch * world
+        ld8 = self.ld8 = lambda n: (n + 7) // 8 * 8           # TMA needs a 16-byte row pitch: pad ld
+        batch = self.batch
+        g = torch.Generator(device=dev)
+
+        def U(*shape, seed=None):
+            if seed is not None:
+                g.manual_seed(seed)
+            return (torch.rand(*shape, generator=g, device=dev, dtype=torch.float32) * 2 - 1).half()
+
+        def operand(rows, cols, lay, which, rot):
+            """Logical (batch, rows, cols) fp16 operand stored row- ('r') or column-major ('c'), ld padded.
+            Sharded batches draw item b from its own seed, so a rank's items do not depend on N."""
+            shape = (rows, ld8(cols)) if lay == "r" else (cols, ld8(rows))
+            if self.sharded:
+                x = torch.stack([U(*shape, seed=(4 << 24) + (rot << 16) + (b << 2) + which)
+                                 for b in range(self.lo, self.hi)]) if batch else \
+                    torch.empty((0,) + shape, dtype=torch.float16, device=dev)
+            else:
+                x = U(batch, *shape, seed=1000 + rank + 7919 * (rot * 4 + which))
+            return x[:, :, :cols] if lay == "r" else x[:, :, :rows].transpose(1, 2)
+
+        set_bytes = max(1, sum(2 * (M * ld8(K) + K * ld8(N)) * batch for _ in layouts))
+        self.n_sets = max(1, min(64, -(-int(3 * 126e6) // set_bytes)))
+        self.sets = [[(lay, operand(M, K, lay[0], 1, r), operand(K, N, lay[1], 2, r)) for lay in layouts]
+                     for r in range(self.n_sets)]
+        self.set_bytes = set_bytes
+        if self.sharded:
+            self.bias = torch.stack([U(N, seed=(4 << 24) + (b << 2) + 3) for b in range(self.lo, self.hi)]) \
+                if batch else torch.empty((0, N), dtype=torch.float16, device=dev)
+        else:
+            self.bias = U(N, seed=1000 + rank + 31)
+        self.scale = (torch.rand(K, generator=g, device=dev) + 0.5) if pro == "scale_k" else None
+        self.C = torch.empty(max(batch, 1), M, ld8(N), dtype=torch.float16, device=dev)[:batch, :, :N]
+        self.step_no = 0
+        self.graphs = None
+
+    def launch(self, A, B):
+        ge = self.ge
+        if self.sharded:
+            from paper_2006_12645_b200 import sharded
+            sharded.sharded_gemm_epilogue_batched(A, B, self.bias, presliced=True, total_batch=self.gbatch,
+                                                  prologue=self.pro, scale=self.scale, out=self.C)
+        elif self.batch == 1:
+            ge.gemm_epilogue(A[0], B[0], self.bias, prologue=self.pro, scale=self.scale, out=self.C[0])
+        else:
+            ge.gemm_epilogue_batched(A, B, self.bias, prologue=self.pro, scale=self.scale, out=self.C)
+
+    def launches_per_step(self):
+        return len(self.layouts) if self.batch > 0 else 0
+
+    def step_eager(self):
+        cur = self.sets[self.step_no % self.n_sets]
+        self.step_no += 1
+        for lay, A, B in cur:
+            self.launch(A, B)
+
+    def capture(self):
+        torch = self.torch
+        self.graphs = []
+        for cur in self.sets:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for lay, A, B in cur:
+                    self.launch(A, B)
+            self.graphs.append(gr)
+
+    def step(self, s):
+        if self.graphs is not None:
+            self.graphs[s % self.n_sets].replay()
+        else:
+            self.step_eager()
+
+    def flop_per_launch(self):
+        return 2.0 * self.M * self.N * self.K * self.batch
+
+
+def time_steps(w, steps, warmup, stream, torch, dist, world, graph=True, clock=None):
+    """W eager warm-up steps, graph capture, then `steps` timed steps bracketed by barrier +
+    synchronize; per-step CUDA events on the launching stream.  Returns (ms total (max over ranks),
+    per-launch kernel ms on this rank, #launches)."""
+    for _ in range(warmup):
+        w.step_eager()
+    torch.cuda.synchronize()
+    if graph:
+        w.capture()
+        for i in range(max(1, warmup)):
+            w.step(i)
+        torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = w.ge.launch_count()
+    ctx = clock if clock is not None else _NullCtx()
+    with ctx:
+        t0.record(stream)
+        for s in range(steps):
+            ev[s][0].record(stream)
+            w.step(s)
+            ev[s][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    n_launch = (w.ge.launch_count() - n0) if w.graphs is None else w.launches_per_step() * steps
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    lps = max(1, w.launches_per_step())
+    kern_ms = sum(a.elapsed_time(b) / lps for a, b in ev) / max(1, steps)
+    if world > 1:
+        tt = torch.tensor([ms], device=w.C.device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return ms, kern_ms, n_launch
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2006_12645_b200 as ge
-    import workloads
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -221,151 +397,51 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     ge.load_library()
-    batch, M, N, K, layouts, pro = WORKLOADS[args.workload]
-    cfg = workload_config(args.workload, world)
-    seed = 1000 + rank
-
-    # ---- synthetic operands (seeded per rank, generated on the device: timing excludes them)
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-    def U(*shape):
-        return (torch.rand(*shape, generator=g, device=dev, dtype=torch.float32) * 2 - 1).half()
-    ld8 = lambda n: (n + 7) // 8 * 8           # TMA needs 16-byte row pitch: pad leading dimensions
-
-    def operand(rows, cols, lay):
-        """Logical (batch, rows, cols) fp16 operand stored row- ('r') or column-major ('c'), ld padded."""
-        if lay == "r":
-            return U(batch, rows, ld8(cols))[:, :, :cols]
-        return U(batch, cols, ld8(rows))[:, :, :rows].transpose(1, 2)
-
-    # Operand sets are rotated between steps so the working set exceeds the 126 MB L2 (no flush
-    # kernel inside the timed region); one set when a single step already streams > 3x L2.
-    set_bytes = sum(2 * (M * ld8(K) + K * ld8(N)) * batch for _ in layouts)
-    n_sets = max(1, min(64, -(-int(3 * 126e6) // set_bytes)))
-    sets = [[(lay, operand(M, K, lay[0]), operand(K, N, lay[1])) for lay in layouts] for _ in range(n_sets)]
-    ops = sets[0]
-    bias = U(N)
-    scale = (torch.rand(K, generator=g, device=dev) + 0.5) if pro == "scale_k" else None
-    C = torch.empty(batch, M, ld8(N), dtype=torch.float16, device=dev)[:, :, :N]
-    cfg["l2"] = (f"{n_sets} operand sets rotated across steps ({n_sets * set_bytes / 1e6:.0f} MB working set > "
+    name = resolve_workload(args.workload, world)
+    w = Workload(name, dev, rank, world, torch, ge)
+    cfg = workload_config(name, world, rank)
+    M, N, K, pro = w.M, w.N, w.K, w.pro
+    cfg["l2"] = (f"{w.n_sets} operand sets rotated across steps ({w.n_sets * w.set_bytes / 1e6:.0f} MB working set > "
                  f"126 MB L2), no flush")
-    if ld8(N) != N or ld8(K) != K or ld8(M) != M:
+    if w.ld8(N) != N or w.ld8(K) != K or w.ld8(M) != M:
         cfg["padding"] = "leading dimensions padded to a multiple of 8 elements (16-byte TMA pitch)"
     stream = torch.cuda.current_stream()
 
-    def launch(lay, A, B):
-        if batch == 1:
-            ge.gemm_epilogue(A[0], B[0], bias, prologue=pro, scale=scale, out=C[0])
-        else:
-            ge.gemm_epilogue_batched(A, B, bias, prologue=pro, scale=scale, out=C)
+    clk = ClockSampler(local)
+    ms, kern_avg_ms, n_launches = time_steps(w, args.steps, args.warmup, stream, torch, dist, world,
+                                             graph=not args.no_graph, clock=clk)
+    flop_step_global = 2.0 * M * N * K * len(w.layouts) * w.gbatch
+    value = flop_step_global * args.steps / (ms * 1e-3) / 1e12
 
-    step_no = [0]
-
-    def step_eager():
-        cur = sets[step_no[0] % n_sets]
-        step_no[0] += 1
-        for lay, A, B in cur:
-            launch(lay, A, B)
-
-    for _ in range(args.warmup):
-        step_eager()
-    torch.cuda.synchronize()
-
-    # A step is replayed from a CUDA graph captured per operand set (the 4 launches are plain
-    # cudaLaunchKernelEx calls on the capturing stream): no host launch overhead in the timed region.
-    graphs = None
-    launches_per_step = len(layouts)
-    if not args.no_graph:
-        graphs = []
-        for cur in sets:
-            gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr):
-                for lay, A, B in cur:
-                    launch(lay, A, B)
-            graphs.append(gr)
-        for i in range(max(1, args.warmup)):
-            graphs[i % n_sets].replay()
+    # ---- optional all-gather of the output shards (off the hot path; algbw / busbw, nccl-tests convention)
+    gather = None
+    if args.gather and w.sharded and world > 1:
+        from paper_2006_12645_b200 import sharded
+        sharded.gather_rows(w.C, w.gbatch)
         torch.cuda.synchronize()
-
-    # ---- timed region
-    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
         dist.barrier()
-    torch.cuda.synchronize()
-    n_launch0 = ge.launch_count()
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for s in range(args.steps):
-            step_ev[s][0].record(stream)
-            if graphs is not None:
-                graphs[s % n_sets].replay()
-            else:
-                step_eager()
-            step_ev[s][1].record(stream)
-        t1.record(stream)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        reps = 5
+        for _ in range(reps):
+            sharded.gather_rows(w.C, w.gbatch)
+        g1.record(stream)
         torch.cuda.synchronize()
-    n_launches = (ge.launch_count() - n_launch0) if graphs is None else launches_per_step * args.steps
-    if world > 1:
-        dist.barrier()
-    ms = t0.elapsed_time(t1)
-    # the step holds only our kernels, back to back: per-launch time = step time / launches
-    kern_ms = [a.elapsed_time(b) / launches_per_step for (a, b) in step_ev]
-    kern_avg_ms = sum(kern_ms) / len(kern_ms)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        gms = g0.elapsed_time(g1) / reps
+        tt = torch.tensor([gms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    flop_per_launch = 2.0 * M * N * K * batch
-    flop_total = flop_per_launch * len(ops) * args.steps * world
-    value = flop_total / (ms * 1e-3) / 1e12
+        gms = float(tt.item())
+        nbytes = w.gbatch * M * N * 2
+        gather = {"bytes": nbytes, "ms": gms, "algbw_gbs": nbytes / (gms * 1e-3) / 1e9,
+                  "busbw_gbs": nbytes / (gms * 1e-3) / 1e9 * (world - 1) / world,
+                  "note": "torch.distributed all_gather_into_tensor (NCCL) of the C shards, timed after the steps"}
 
-    # ---- end to end through the host-buffer C-ABI entry point
+    # ---- end to end through the host-buffer C-ABI entry point (this rank's items)
     e2e = None
-    if args.e2e_steps > 0:
-        def host_copy(x, lay):
-            """Pinned host copy of a logical (batch, rows, cols) operand, same layout and padded ld."""
-            rows, cols = x.shape[1], x.shape[2]
-            if lay == "r":
-                st_ = torch.empty(batch, rows, ld8(cols), dtype=torch.float16).pin_memory()
-                st_[:, :, :cols] = x.cpu()
-                return st_[:, :, :cols], st_.numel() * 2
-            st_ = torch.empty(batch, cols, ld8(rows), dtype=torch.float16).pin_memory()
-            st_[:, :, :rows] = x.transpose(1, 2).cpu()
-            return st_[:, :, :rows].transpose(1, 2), st_.numel() * 2
-        hA = [host_copy(A, lay[0]) for lay, A, B in ops]
-        hB = [host_copy(B, lay[1]) for lay, A, B in ops]
-        Ah, Bh = [x for x, _ in hA], [x for x, _ in hB]
-        bh = bias.cpu().pin_memory()
-        sh = scale.cpu().pin_memory() if scale is not None else None
-        Ch = torch.empty(batch, M, ld8(N), dtype=torch.float16).pin_memory()[:, :, :N]
-
-        def e2e_step():
-            for i in range(len(ops)):
-                ge.gemm_epilogue_host(Ah[i], Bh[i], bh, prologue=pro, scale=sh, out=Ch)
-        e2e_step()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
-        h2d = sum(na + nb + bh.numel() * 2 + (sh.numel() * 4 if sh is not None else 0)
-                  for (_, na), (_, nb) in zip(hA, hB))
-        d2h = len(ops) * batch * M * N * 2
-        e2e = {"value": flop_per_launch * len(ops) * args.e2e_steps * world / (ems * 1e-3) / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-               "path": "gemm_epilogue_host (C ABI, pinned host buffers)"}
-        ge.load_library().ge_release_workspace()
+    if args.e2e_steps > 0 and w.batch > 0:
+        e2e = run_e2e(args, w, torch, dist, world, stream, dev)
+        cfg_e2e_flop = 2.0 * M * N * K * len(w.layouts) * w.gbatch
+        e2e["value"] = cfg_e2e_flop * args.e2e_steps / (e2e.pop("ms") * 1e-3) / 1e12
 
     clocks = clk.summary()
     if world > 1:
@@ -375,28 +451,55 @@ def run_ours(args):
         clocks["per_rank_sm_mhz"] = [c.get("sm_mhz") for c in allc]
         clocks["reasons"] = sorted({r for c in allc for r in c.get("reasons", [])})
 
+    # ---- N = 1 point of the N > 1 default (scale series), measured in the same run
+    scale_series = None
+    if world == 1 and args.workload == "auto" and not args.no_scale_series:
+        ws = Workload("batched64x2048", dev, 0, 1, torch, ge)
+        sms_, skm_, _ = time_steps(ws, min(args.steps, 10), 3, stream, torch, dist, 1, graph=not args.no_graph)
+        fl = 2.0 * ws.M * ws.N * ws.K * ws.gbatch * min(args.steps, 10)
+        scale_series = {"workload": "batched64x2048 (global batch 64 sharded by batch; the default at N > 1)",
+                        "value_n1": fl / (sms_ * 1e-3) / 1e12, "unit": UNIT,
+                        "kernel_avg_ms": skm_, "steps": min(args.steps, 10)}
+        del ws
+
     if rank == 0:
-        peak, peak_sus, peak_src = measured_peak()
-        achieved = flop_per_launch / (kern_avg_ms * 1e-3) / 1e12
-        traffic, tsrc = ncu_traffic(args.workload)
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic,
-                    "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops; fp16 = bf16 nominal)",
-                    "frac_of_sustained": (achieved / peak_sus) if peak_sus else None,
-                    "frac_of_spec_2250": achieved / 2250.0,
-                    "kernel": "ge_fused_kernel (one launch per GEMM)",
-                    "kernel_avg_ms": kern_avg_ms,
-                    "launch_mode": "CUDA graph replay per step" if graphs is not None else "eager",
-                    "traffic_source": tsrc}
+        peak, peak_sus, hbm, peak_src = measured_peaks()
+        flop_launch = w.flop_per_launch()
+        bytes_launch = algorithmic_bytes(w.batch, M, N, K, pro)
+        ai = flop_launch / max(1.0, bytes_launch)
+        ridge = peak * 1e12 / (hbm * 1e9)
+        traffic, tsrc = ncu_traffic(name)
+        common = {"kernel": "ge_fused_kernel (one launch per GEMM / batch)", "kernel_avg_ms": kern_avg_ms,
+                  "launch_mode": "CUDA graph replay per step" if not args.no_graph else "eager",
+                  "traffic": traffic, "traffic_source": tsrc,
+                  "algorithmic_flop_per_launch": flop_launch, "algorithmic_bytes_per_launch": bytes_launch,
+                  "arithmetic_intensity": ai, "ridge_flop_per_byte": ridge}
+        if ai < ridge:
+            # HBM-bound shape: GB/s of algorithmic bytes against the measured copy bandwidth
+            achieved = bytes_launch / (kern_avg_ms * 1e-3) / 1e9
+            roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                        "peak_source": f"{peak_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                        "tflops": flop_launch / (kern_avg_ms * 1e-3) / 1e12, **common}
+        else:
+            achieved = flop_launch / (kern_avg_ms * 1e-3) / 1e12
+            roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak,
+                        "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops; fp16 = bf16 nominal)",
+                        "frac_of_sustained": (achieved / peak_sus) if peak_sus else None,
+                        "frac_of_spec_2250": achieved / 2250.0, **common}
         comparators = None
-        if not args.no_comparators and batch == 1:
-            comparators = compare_torch(torch, sets, bias, M, N, K, stream, iters=args.steps * len(layouts))
+        if not args.no_comparators and w.batch == 1:
+            comparators = compare_torch(torch, w, stream, iters=args.steps * len(w.layouts))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f16", "accumulate": "f32",
-                "data": "synthetic (seeded U(-1,1) fp16)", "config": cfg,
+                "scaling": "strong" if w.sharded else "weak", "vs_baseline": None, "dtype": "f16",
+                "accumulate": "f32", "data": "synthetic (seeded U(-1,1) fp16)", "config": cfg,
                 "roofline": roofline, "e2e": e2e, "gpu_launches": n_launches, "clocks": clocks,
                 "comparators": comparators}
+        if gather:
+            line["gather"] = gather
+        if scale_series:
+            line["scale_series"] = scale_series
         if not args.no_cpu_baseline:
             rate, cores, desc, _ = oracle_rate(M, N, K, seed=7, budget_s=12.0)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
@@ -407,19 +510,84 @@ def run_ours(args):
     return 0
 
 
-def compare_torch(torch, sets, bias, M, N, K, stream, iters=10):
+def run_e2e(args, w, torch, dist, world, stream, dev):
+    """The same step through the host-buffer C-ABI entry (gemm_epilogue_host): pinned host inputs
+    copied in and C copied out inside the timed region; this rank's items."""
+    ge, ld8, batch = w.ge, w.ld8, w.batch
+
+    def host_copy(x, lay):
+        """Pinned host copy of a logical (batch, rows, cols) operand, same layout and padded ld."""
+        rows, cols = x.shape[1], x.shape[2]
+        if lay == "r":
+            st_ = torch.empty(batch, rows, ld8(cols), dtype=torch.float16).pin_memory()
+            st_[:, :, :cols] = x.cpu()
+            return st_[:, :, :cols], st_.numel() * 2
+        st_ = torch.empty(batch, cols, ld8(rows), dtype=torch.float16).pin_memory()
+        st_[:, :, :rows] = x.transpose(1, 2).cpu()
+        return st_[:, :, :rows].transpose(1, 2), st_.numel() * 2
+    ops = w.sets[0]
+    hA = [host_copy(A, lay[0]) for lay, A, B in ops]
+    hB = [host_copy(B, lay[1]) for lay, A, B in ops]
+    Ah, Bh = [x for x, _ in hA], [x for x, _ in hB]
+    bh = w.bias.cpu().pin_memory()
+    sh = w.scale.cpu().pin_memory() if w.scale is not None else None
+    Ch = torch.empty(batch, w.M, ld8(w.N), dtype=torch.float16).pin_memory()[:, :, :w.N]
+
+    def e2e_step():
+        for i in range(len(ops)):
+            if batch == 1:
+                ge.gemm_epilogue_host(Ah[i][0], Bh[i][0], bh, prologue=w.pro, scale=sh, out=Ch[0])
+            else:
+                ge.gemm_epilogue_host(Ah[i], Bh[i], bh, prologue=w.pro, scale=sh, out=Ch)
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ems = float(tt.item())
+    h2d = sum(na + nb + bh.numel() * 2 + (sh.numel() * 4 if sh is not None else 0) for (_, na), (_, nb) in zip(hA, hB))
+    d2h = len(ops) * batch * w.M * w.N * 2
+    ge.load_library().ge_release_workspace()
+    return {"ms": ems, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": args.e2e_steps, "path": "gemm_epilogue_host (C ABI, pinned host buffers)"}
+
+
+def compare_torch(torch, w, stream, iters=10):
     """Library reference points on the same box and the same rotating operand sets (not the product):
     torch unfused matmul + add + relu (cuBLAS + 2 elementwise kernels, the paper's baseline shape,
     PAPER.md:1255-1260), torch._addmm_activation (cuBLASLt bias+ReLU epilogue) and plain
-    torch.matmul.  Each is replayed from CUDA graphs like our step; first layout of each set."""
+    torch.matmul.  Each is replayed from CUDA graphs like our step; first layout of each set.
+    Like-for-like alignment: when N is not a multiple of 8, the library computes the padded
+    N' = ld8(N) columns of the same padded operand storage we read, so its C rows are 16-byte
+    aligned like ours (TFLOP/s still counts the logical 2MNK)."""
     out = {}
+    M, N, K = w.M, w.N, w.K
     fl = 2.0 * M * N * K
+    Np = w.ld8(N)
+    lay0 = w.sets[0][0][0]
+    pad = Np != N and lay0[1] == "r"
+    bias = w.bias if not pad else torch.cat([w.bias, torch.zeros(Np - N, dtype=w.bias.dtype, device=w.bias.device)])
+
+    def operands(cur):
+        lay, A, B = cur[0]
+        a, b = A[0], B[0]
+        if pad:
+            b = torch.as_strided(b, (K, Np), (b.stride(0), 1))     # the padded storage row pitch (ld8(N))
+        return a, b
 
     def t(fn, it=iters):
         graphs = []
-        for cur in sets:
-            lay, A, B = cur[0]
-            a, b = A[0], B[0]
+        for cur in w.sets:
+            a, b = operands(cur)
             fn(a, b)
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
@@ -439,9 +607,10 @@ def compare_torch(torch, sets, bias, M, N, K, stream, iters=10):
         out["torch_unfused_matmul_add_relu"] = fl / t(lambda a, b: torch.relu_(torch.matmul(a, b).add_(bias))) / 1e12
         out["torch_matmul_only"] = fl / t(lambda a, b: torch.matmul(a, b)) / 1e12
         out["cublaslt_addmm_relu"] = fl / t(lambda a, b: torch._addmm_activation(bias, a, b)) / 1e12
-        out["layout"] = sets[0][0][0]
+        out["layout"] = lay0
+        out["ldc"] = Np if pad else N
         out["protocol"] = (f"CUDA graph replay, same rotating operand sets, {iters} launches each "
-                           "(as many as our timed region)")
+                           "(as many as our timed region)" + ("; N padded to ld8(N) for 16-B aligned C rows" if pad else ""))
     except Exception as e:  # pragma: no cover
         out["error"] = str(e)
     return out

@@ -102,12 +102,14 @@ typedef struct {
     int32_t stream_k;               /* 0 = heuristic (stream-K tail or split-K); 1 = off (data-parallel
                                        tiles only); 2 = stream-K (never split-K) whenever the last
                                        wave is partial */
-    void* workspace;                /* optional device workspace for stream-K partials (see ge_plan's
+    void* workspace;                /* optional device workspace for stream-K partials (size: ge_plan's
                                        workspace_bytes); 16-byte aligned, ZERO-FILLED before its first
                                        use and left zero-filled by every launch; must not be shared by
-                                       launches that may run concurrently.  NULL = library-managed
-                                       per-device buffer (then stream-K launches on different streams of
-                                       one device must not run concurrently; stream_k = 1 disables it). */
+                                       launches that may run concurrently.  NULL (or smaller than the
+                                       planned size) = no stream-K: the heuristic then plans data-parallel
+                                       or split-K tiles only (the library never allocates device memory
+                                       on the device-pointer entry points); stream_k = 2 with no or too
+                                       small a workspace is GE_ERR_INVALID_VALUE. */
     int64_t workspace_bytes;
     int32_t multicast;              /* 0 = heuristic; 1 = off; 2 = force clusters of two CTA pairs stacked
                                        along M (512 x tile_n tiles) whose B tiles are loaded once and
@@ -171,8 +173,10 @@ ge_status gemm2_epilogue(int64_t M, int64_t N, int64_t K1, int64_t K2,
  * bandwidth and copy/compute overlap; pageable works).  The call copies B (and bias, scale) to
  * a library-owned device workspace, then streams A and C in blocks (row blocks, or batch items)
  * on library copy/compute streams so each block's kernel and C read-back overlap the next
- * block's upload; it is ordered after prior work on `stream` and synchronizes before returning.  The workspace grows on demand, is kept per device for reuse and is
- * released by ge_release_workspace().  Operand alignment rules apply to ld/strides only.
+ * block's upload; it is ordered after prior work on `stream` and synchronizes before returning.
+ * This entry point (only) allocates: the workspace (operands, C and a stream-K area) grows on
+ * demand, is kept per device for reuse and is released by ge_release_workspace().  Operand
+ * alignment rules apply to ld/strides only.
  */
 ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K,
                              int32_t layoutA, int32_t layoutB,
@@ -209,9 +213,12 @@ const char* ge_last_error_detail(void);
  * tile_n, cta_group, pipeline stages, the number of output tiles, how many of them run
  * stream-K (the last partial wave's tiles, whose K range is split evenly across all clusters;
  * partial sums are reduced in fixed order, so results stay run-to-run deterministic), the
- * split-K factor (split_k > 1: every tile is computed by split_k clusters, one K-slice each, and
- * the fp32 partials are reduce-scattered by column slice through the workspace in fixed order;
- * only for few, long tiles) and the workspace bytes either needs.  Any output pointer may be NULL.
+ * split-K factor (split_k > 1: every tile is computed by a cluster of split_k CTAs, one K-slice
+ * each, and the fp32 partials are reduce-scattered through distributed shared memory in fixed
+ * order -- no workspace; only for few, long tiles) and the stream-K workspace bytes.  The plan is
+ * the one a launch makes when given opt->workspace of at least *workspace_bytes (without one, a
+ * launch re-plans with stream-K off).  The option checks of the launch entry points apply
+ * (GE_ERR_INVALID_VALUE for invalid combinations).  Any output pointer may be NULL.
  */
 ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                   const ge_options* opt, int32_t num_sms,
@@ -220,6 +227,11 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
 
 /* Number of fused kernels this library has launched in this process (for launch accounting). */
 uint64_t ge_launch_count(void);
+
+/* Tensor-map cache counters of this process: maps reused / encoded with
+ * cuTensorMapEncodeTiled.  The cache memoises encodings by (address, dims, strides, box, swizzle,
+ * type) and owns nothing.  Either pointer may be NULL. */
+void ge_tensor_map_cache_stats(uint64_t* hits, uint64_t* misses);
 
 /*
  * Diagnostics: when the process runs with GE_DEBUG_STATS=1, every launch records per-CTA

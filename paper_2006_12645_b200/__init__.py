@@ -103,6 +103,8 @@ def load_library():
     lib.ge_debug_read.argtypes = [P, I32]
     lib.ge_version.restype = ctypes.c_char_p
     lib.ge_version.argtypes = []
+    lib.ge_tensor_map_cache_stats.restype = None
+    lib.ge_tensor_map_cache_stats.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     _lib = lib
     return lib
 
@@ -197,6 +199,63 @@ def _op(op: str, bias) -> int:
     return EPI[op]
 
 
+def _check_tensors(M, N, K, *, ops, bias=None, bias_mode="row", scale=None, out=None, batch=None, host=False):
+    """Argument checks the C ABI cannot make (it sees raw pointers): dtypes, shapes against M/N/K
+    and the bias mode, and that every tensor lives on one CUDA device (or on the host for the
+    host-buffer entry).  Raises ValueError; nothing is launched."""
+    dev = None
+    def where(name, t):
+        nonlocal dev
+        if host:
+            if t.is_cuda:
+                raise ValueError(f"{name} must be a host (CPU) tensor for gemm_epilogue_host")
+            return
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"{name} is on {t.device}, expected {dev}")
+    for name, t in ops:
+        if t.dtype != torch.float16:
+            raise ValueError(f"{name} must be float16, got {t.dtype}")
+        where(name, t)
+    lead = () if batch is None else (batch,)
+    if bias is not None:
+        if bias.dtype != torch.float16:
+            raise ValueError(f"bias must be float16, got {bias.dtype}")
+        where("bias", bias)
+        if bias_mode not in BIAS_MODE:
+            raise ValueError(f"bias_mode must be one of {sorted(BIAS_MODE)}")
+        if bias_mode == "full":
+            ok = bias.dim() in ((2, 3) if batch is not None else (2,)) and bias.shape[-2] == M and bias.shape[-1] >= N
+            if ok and bias.dim() == 3:
+                ok = bias.shape[0] == batch
+            if not ok:
+                raise ValueError(f"full bias must be (M, >=N){' or (batch, M, >=N)' if batch is not None else ''}, "
+                                 f"got {tuple(bias.shape)}")
+        else:
+            L = N if bias_mode == "row" else M
+            ok = (bias.dim() == 1 and bias.shape[0] == L) or \
+                 (batch is not None and bias.dim() == 2 and tuple(bias.shape) == (batch, L))
+            if not ok:
+                raise ValueError(f"{bias_mode} bias must have length {'N' if bias_mode == 'row' else 'M'} = {L}"
+                                 f"{' (or shape (batch, ' + str(L) + '))' if batch is not None else ''}, got "
+                                 f"{tuple(bias.shape)}")
+    if scale is not None:
+        if scale.dtype != torch.float32:
+            raise ValueError(f"scale must be float32, got {scale.dtype}")
+        if scale.dim() != 1 or scale.numel() < K or scale.stride(0) != 1:
+            raise ValueError(f"scale must be a contiguous 1-D tensor of length >= K = {K}")
+        where("scale", scale)
+    if out is not None:
+        if out.dtype not in (torch.float16, torch.float32):
+            raise ValueError(f"out must be float16 or float32, got {out.dtype}")
+        if tuple(out.shape) != lead + (M, N):
+            raise ValueError(f"out must have shape {lead + (M, N)}, got {tuple(out.shape)}")
+        where("out", out)
+
+
 def _bias_ld(bias, bias_mode):
     if bias is None:
         return 0, 0
@@ -229,6 +288,9 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     K2, N = B.shape
     if K2 != K:
         raise ValueError(f"inner dimensions differ: A is {tuple(A.shape)}, B is {tuple(B.shape)}")
+    if prologue == "scale_k" and scale is None:
+        raise ValueError("prologue 'scale_k' needs scale")
+    _check_tensors(M, N, K, ops=(("A", A), ("B", B)), bias=bias, bias_mode=bias_mode, scale=scale, out=out)
     la, lda = layout_of(A)
     lb, ldb = layout_of(B)
     if out is None:
@@ -259,6 +321,7 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
     K2 = P.shape[1]
     if B.shape[0] != K1 or P.shape[0] != M or Q.shape != (K2, N):
         raise ValueError("shapes of A.B and P.Q disagree")
+    _check_tensors(M, N, K1, ops=(("A", A), ("B", B), ("P", P), ("Q", Q)), bias=bias, bias_mode=bias_mode, out=out)
     la, lda = layout_of(A)
     lb, ldb = layout_of(B)
     lp, ldp = layout_of(P)
@@ -267,6 +330,8 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
         raise ValueError("P must have A's layout and Q must have B's layout")
     if out is None:
         out = torch.empty((M, N), dtype=out_dtype, device=A.device)
+    if out.stride(-1) != 1 and N > 1:
+        raise ValueError("out must be row-major")
     ldbias, _ = _bias_ld(bias, bias_mode)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, None, None, out.dtype, tile_n, cta_group, stream_k,
@@ -278,13 +343,17 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
     return out
 
 
-def _batched_args(A, B, bias, bias_mode, out):
+def _batched_args(A, B, bias, bias_mode, out, scale=None, host=False):
     if A.dim() != 3 or B.dim() != 3:
         raise ValueError("batched operands are (batch, rows, cols)")
     batch, M, K = A.shape
     _, K2, N = B.shape
     if K2 != K or B.shape[0] != batch:
         raise ValueError("batched shapes disagree")
+    _check_tensors(M, N, K, ops=(("A", A), ("B", B)), bias=bias, bias_mode=bias_mode, scale=scale,
+                   out=(out if out is None or out.dim() == 3 else out.unsqueeze(0)), batch=batch, host=host)
+    if out is not None and out.stride(-1) != 1 and N > 1:
+        raise ValueError("out must be row-major")
     la, lda = layout_of(A)
     lb, ldb = layout_of(B)
     ldbias, sbias = _bias_ld(bias, bias_mode)
@@ -299,7 +368,9 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
     """Strided-batched form: A (b, M, K), B (b, K, N), bias (N,)/(b, N) [row], (M,)/(b, M) [col],
     (M, ld)/(b, M, ld) [full]; a 1-D/2-D bias is shared by every item.  One persistent launch."""
     lib = load_library()
-    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A, B, bias, bias_mode, out)
+    if prologue == "scale_k" and scale is None:
+        raise ValueError("prologue 'scale_k' needs scale")
+    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A, B, bias, bias_mode, out, scale)
     if out is None:
         out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
     sh = _stream(stream, A.get_device())
@@ -322,7 +393,11 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
     lib = load_library()
     A3 = A if A.dim() == 3 else A.unsqueeze(0)
     B3 = B if B.dim() == 3 else B.unsqueeze(0)
-    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A3, B3, bias, bias_mode, out)
+    if prologue == "scale_k" and scale is None:
+        raise ValueError("prologue 'scale_k' needs scale")
+    out3 = None if out is None else (out if out.dim() == 3 else out.unsqueeze(0))
+    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A3, B3, bias, bias_mode, out3, scale,
+                                                                            host=True)
     if out is None:
         out = torch.empty((batch, M, N) if A.dim() == 3 else (M, N), dtype=out_dtype,
                           pin_memory=A.is_pinned())
@@ -357,6 +432,13 @@ def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: i
 
 def launch_count() -> int:
     return int(load_library().ge_launch_count())
+
+
+def tensor_map_cache_stats() -> dict:
+    """{"hits": maps reused, "misses": maps encoded} of the library's tensor-map cache."""
+    h, m = ctypes.c_uint64(), ctypes.c_uint64()
+    load_library().ge_tensor_map_cache_stats(ctypes.byref(h), ctypes.byref(m))
+    return {"hits": h.value, "misses": m.value}
 
 
 def debug_stats(max_ctas: int = 148):

@@ -110,17 +110,11 @@ int act_of(int32_t op) {
                                                   : (op & GE_EPI_TANH) ? ge::ACT_TANH : ge::ACT_NONE;
 }
 
-// Normalises ld/stride defaults in place and checks everything that can be checked on the host.
-ge_status validate(Args& a) {
-    char buf[256];
-    if (a.batch < 0 || a.M < 0 || a.N < 0 || a.K < 0)
-        return fail(GE_ERR_INVALID_VALUE, "negative size");
-    if (a.M > kMaxDim || a.N > kMaxDim || a.K > kMaxDim || a.batch > kMaxDim)
-        return fail(GE_ERR_INVALID_VALUE, "size exceeds 2^31-1");
+// Option and enum checks shared by validate() and ge_plan() (no pointers involved).
+ge_status validate_options(const Args& a) {
+    const ge_options& o = a.o;
     if ((a.la != GE_ROW_MAJOR && a.la != GE_COL_MAJOR) || (a.lb != GE_ROW_MAJOR && a.lb != GE_COL_MAJOR))
         return fail(GE_ERR_INVALID_VALUE, "layout must be GE_ROW_MAJOR or GE_COL_MAJOR");
-    if (!op_valid(a.op)) return fail(GE_ERR_INVALID_VALUE, "bad epilogue op (see ge_epilogue_op flags)");
-    const ge_options& o = a.o;
     if (o.bias_mode < GE_BIAS_ROW || o.bias_mode > GE_BIAS_FULL) return fail(GE_ERR_INVALID_VALUE, "bad bias_mode");
     if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_RELU) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
     if (o.out_dtype != GE_OUT_F16 && o.out_dtype != GE_OUT_F32) return fail(GE_ERR_INVALID_VALUE, "bad out_dtype");
@@ -138,6 +132,23 @@ ge_status validate(Args& a) {
         return fail(GE_ERR_INVALID_VALUE, "multicast = 2 needs no prologue, stream_k != 2, cta_group 0/2, tile_n 0/256/512");
     if (o.workspace_bytes < 0 || (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 15)))
         return fail(GE_ERR_INVALID_VALUE, "workspace must be 16-byte aligned with a non-negative size");
+    return GE_OK;
+}
+
+// Normalises ld/stride defaults in place and checks everything that can be checked on the host.
+ge_status validate(Args& a) {
+    char buf[256];
+    if (a.batch < 0 || a.M < 0 || a.N < 0 || a.K < 0)
+        return fail(GE_ERR_INVALID_VALUE, "negative size");
+    if (a.M > kMaxDim || a.N > kMaxDim || a.K > kMaxDim || a.batch > kMaxDim)
+        return fail(GE_ERR_INVALID_VALUE, "size exceeds 2^31-1");
+    if ((a.la != GE_ROW_MAJOR && a.la != GE_COL_MAJOR) || (a.lb != GE_ROW_MAJOR && a.lb != GE_COL_MAJOR))
+        return fail(GE_ERR_INVALID_VALUE, "layout must be GE_ROW_MAJOR or GE_COL_MAJOR");
+    if (!op_valid(a.op)) return fail(GE_ERR_INVALID_VALUE, "bad epilogue op (see ge_epilogue_op flags)");
+    {
+        const ge_status so = validate_options(a);
+        if (so != GE_OK) return so;
+    }
     // packed defaults
     const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
     const int64_t minlda = arow ? a.K : a.M, minldb = brow ? a.N : a.K;
@@ -291,7 +302,9 @@ const SplitCap* split_capacity() {
     return &c;
 }
 
-Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
+// sk_allowed: a stream-K workspace is available (the caller passed one); without it the planner
+// considers only data-parallel and split-K tiles (the library never allocates on the device entry points).
+Plan make_plan(const Args& a, int sms, const SplitCap* cap, bool sk_allowed) {
     // Cost model in SM cycles, calibrated on B200:
     //   one 64-deep k-block of a 128 x BN per-SM tile: 128*BN*64*2 / (8192 flop/clk * eff);
     //   the single-buffered 256 x 512 tile exposes part of its accumulator drain per tile;
@@ -329,7 +342,7 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap = nullptr) {
         int64_t sk = 0;
         // stream-K for the last partial wave (double-buffered accumulators only)
         const int64_t rem = tiles % conc;
-        const bool sk_ok = bn <= 256 && rem != 0 && nkb >= 2 && a.o.stream_k != 1;
+        const bool sk_ok = sk_allowed && bn <= 256 && rem != 0 && nkb >= 2 && a.o.stream_k != 1;
         if (sk_ok) {
             const double share = static_cast<double>(tiles / conc) * nkb + static_cast<double>(rem) * nkb / conc;
             // measured: the owner reads one partial per contributor and every cluster's share ends at
@@ -418,39 +431,6 @@ size_t sk_workspace_bytes(const Plan& pl) {
     return pl.splits ? 0 : ctas * 128 * pl.bn * 4 + ctas * 4;       // split-K reduces in DSMEM
 }
 
-struct SkWorkspace {
-    void* ptr = nullptr;
-    size_t bytes = 0;
-};
-std::mutex g_sk_mu;
-SkWorkspace g_sk[64];
-
-// Library-managed stream-K workspace of the current device (used when the caller passes none).
-void* sk_library_workspace(size_t need, cudaStream_t st) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_sk_mu);
-    SkWorkspace& w = g_sk[dev & 63];
-    if (w.bytes >= need) return w.ptr;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cap);
-    if (cap != cudaStreamCaptureStatusNone) return nullptr;       // cannot allocate while capturing
-    if (w.ptr) {
-        cudaDeviceSynchronize();
-        cudaFree(w.ptr);
-        w.ptr = nullptr;
-        w.bytes = 0;
-    }
-    if (cudaMalloc(&w.ptr, need) != cudaSuccess || cudaMemset(w.ptr, 0, need) != cudaSuccess) {
-        cudaGetLastError();
-        w.ptr = nullptr;
-        return nullptr;
-    }
-    cudaDeviceSynchronize();
-    w.bytes = need;
-    return w.ptr;
-}
-
 // Raster group: tiles are walked in groups of `group_m` tile-rows so the tiles in flight share
 // A panels (along n) and B panels (along m) in L2.  GE_GROUP_M overrides (tuning only).
 int group_m_for(const Plan& pl, const Args& a, int sms) {
@@ -463,22 +443,27 @@ int group_m_for(const Plan& pl, const Args& a, int sms) {
     return 16;
 }
 
-// Diagnostics (env GE_DEBUG_STATS=1): a zeroed per-CTA counter buffer handed to the kernel.
-unsigned long long* g_dbg = nullptr;
-int g_dbg_ctas = 0;
+// Diagnostics (env GE_DEBUG_STATS=1, debug build): a zeroed per-CTA counter buffer per device.
+unsigned long long* g_dbg[64] = {};
+int g_dbg_ctas[64] = {};
+int g_dbg_last = -1;                    // device of the last launch (read by ge_debug_read)
 unsigned long long* debug_buffer(int sms) {
     static const bool on = getenv("GE_DEBUG_STATS") != nullptr;
     if (!on) return nullptr;
-    if (!g_dbg) {
-        if (cudaMalloc(&g_dbg, sizeof(unsigned long long) * 16 * sms) != cudaSuccess) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 63;
+    if (!g_dbg[dev]) {
+        if (cudaMalloc(&g_dbg[dev], sizeof(unsigned long long) * 16 * sms) != cudaSuccess) {
             cudaGetLastError();
-            g_dbg = nullptr;
+            g_dbg[dev] = nullptr;
             return nullptr;
         }
-        g_dbg_ctas = sms;
+        g_dbg_ctas[dev] = sms;
     }
-    cudaMemset(g_dbg, 0, sizeof(unsigned long long) * 16 * g_dbg_ctas);
-    return g_dbg;
+    cudaMemset(g_dbg[dev], 0, sizeof(unsigned long long) * 16 * g_dbg_ctas[dev]);
+    g_dbg_last = dev;
+    return g_dbg[dev];
 }
 
 // ------------------------------------------------------------------ tensor maps
@@ -501,10 +486,63 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// Tensor-map cache: an encoded CUtensorMap depends only on the encode
+// arguments (address, dims, strides, box, swizzle, type), so maps are memoised in a small
+// direct-mapped table keyed by exactly those; repeated calls on the same buffers skip
+// cuTensorMapEncodeTiled.  Entries own nothing: a freed and re-allocated buffer at the same address
+// with the same geometry encodes to the same bytes.  Guarded by a mutex (calls are thread-safe).
+struct MapKey {
+    uint64_t ptr, inner, outer, batch, ld, stride;
+    uint32_t box_inner, box_outer, dt, es, swz, pad;
+    bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapEntry {
+    bool valid = false;
+    MapKey key;
+    CUtensorMap map;
+};
+constexpr int kMapSlots = 256;
+std::mutex g_map_mu;
+MapEntry g_maps[kMapSlots];
+std::atomic<uint64_t> g_map_hits{0}, g_map_misses{0};
+
+uint64_t map_hash(const MapKey& k) {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(&k);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof(MapKey) / 8; ++i) {
+        h ^= w[i];
+        h *= 1099511628211ull;
+        h ^= h >> 29;
+    }
+    return h;
+}
+
 // 3-D map {inner, outer, batch} with 128-B swizzle; OOB elements load as zero, stores clip.
 bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, int64_t inner, int64_t outer,
               int64_t batch, int64_t ld, int64_t stride, uint32_t box_inner, uint32_t box_outer,
               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+    MapKey key;
+    std::memset(&key, 0, sizeof key);
+    key.ptr = reinterpret_cast<uint64_t>(ptr);
+    key.inner = static_cast<uint64_t>(inner);
+    key.outer = static_cast<uint64_t>(outer);
+    key.batch = static_cast<uint64_t>(batch);
+    key.ld = static_cast<uint64_t>(ld);
+    key.stride = static_cast<uint64_t>(batch > 1 ? stride : 0);
+    key.box_inner = box_inner;
+    key.box_outer = box_outer;
+    key.dt = static_cast<uint32_t>(dt);
+    key.es = static_cast<uint32_t>(es);
+    key.swz = static_cast<uint32_t>(swz);
+    MapEntry& slot = g_maps[map_hash(key) % kMapSlots];
+    {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        if (slot.valid && slot.key == key) {
+            *m = slot.map;
+            g_map_hits.fetch_add(1, std::memory_order_relaxed);
+            return true;
+        }
+    }
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)batch};
@@ -516,7 +554,13 @@ bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, i
     CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    if (r != CUDA_SUCCESS) return false;
+    g_map_misses.fetch_add(1, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    slot.valid = true;
+    slot.key = key;
+    slot.map = *m;
+    return true;
 }
 
 ge_status launch(Args& a, cudaStream_t st) {
@@ -526,7 +570,15 @@ ge_status launch(Args& a, cudaStream_t st) {
     int sms = 0;
     s = device_info(&sms);
     if (s != GE_OK) return s;
-    const Plan pl = make_plan(a, sms, split_capacity());
+    // Stream-K needs the caller's workspace (header: no device allocation on this entry point)
+    const bool have_ws = a.o.workspace != nullptr;
+    if (a.o.stream_k == 2 && !have_ws)
+        return fail(GE_ERR_INVALID_VALUE, "stream_k = 2 needs a workspace (size: ge_plan's workspace_bytes)");
+    Plan pl = make_plan(a, sms, split_capacity(), have_ws);
+    if (pl.sk_tiles && static_cast<size_t>(a.o.workspace_bytes) < sk_workspace_bytes(pl)) {
+        if (a.o.stream_k == 2) return fail(GE_ERR_INVALID_VALUE, "workspace smaller than ge_plan's workspace_bytes");
+        pl = make_plan(a, sms, split_capacity(), false);
+    }
     const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
     const bool a_mn = !arow, b_mn = brow;          // row-major A is K-major; row-major B is N(MN)-major
     const bool f32 = a.o.out_dtype == GE_OUT_F32;
@@ -604,14 +656,17 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.c_tma = c_tma ? 1 : 0;
     p.c_vec = c_tma ? 1 : 0;                      // same alignment conditions as the TMA store
 
+#if GE_DBG
+    // diagnostics build only (libgemm_epilogue_dbg.so): counters and timing experiments
     p.dbg = debug_buffer(sms);
     static const int noload = getenv("GE_DEBUG_NOLOAD") ? 1 : 0;   // timing experiment only
     p.dbg_noload = noload;
     static const int dflags = getenv("GE_DEBUG_FLAGS") ? atoi(getenv("GE_DEBUG_FLAGS")) : 0;   // experiments only
     p.dbg_flags = dflags;
     if (dflags & 4) p.c_tma = 0;                  // experiment: st.global epilogue instead of TMA stores
+#endif
 
-    // stream-K (last partial wave split across all clusters) when a workspace is available
+    // stream-K (last partial wave split across all clusters) in the caller's workspace
     Plan plan = pl;
     p.dp_tiles = plan.tiles;
     p.sk_units = 0;
@@ -619,22 +674,11 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.sk_flags = nullptr;
     p.splits = plan.splits;
     if (plan.sk_tiles) {
-        const size_t need = sk_workspace_bytes(plan);
-        void* ws = nullptr;
-        if (a.o.workspace) {
-            if (static_cast<size_t>(a.o.workspace_bytes) >= need) ws = a.o.workspace;
-        } else {
-            ws = sk_library_workspace(need, st);
-        }
-        if (ws) {
-            const size_t ctas = static_cast<size_t>(plan.clusters * plan.cg);
-            p.sk_ws = static_cast<float*>(ws);
-            p.sk_flags = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + ctas * 128 * plan.bn * 4);
-            p.dp_tiles = plan.tiles - plan.sk_tiles;
-            p.sk_units = plan.sk_tiles * p.num_k_blocks;
-        } else {
-            plan.clusters = std::min<int64_t>(plan.tiles, sms / plan.cg);     // data-parallel fallback
-        }
+        const size_t ctas = static_cast<size_t>(plan.clusters * plan.cg);
+        p.sk_ws = static_cast<float*>(a.o.workspace);
+        p.sk_flags = reinterpret_cast<unsigned int*>(static_cast<char*>(a.o.workspace) + ctas * 128 * plan.bn * 4);
+        p.dp_tiles = plan.tiles - plan.sk_tiles;
+        p.sk_units = plan.sk_tiles * p.num_k_blocks;
     }
     const int grid = static_cast<int>(std::max<int64_t>(plan.clusters, 1) * plan.cg * (plan.mc ? 2 : 1));
     cudaError_t e;
@@ -796,7 +840,10 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
     const int64_t nS = (a.o.prologue == GE_PRO_SCALE_K && a.K) ? a.K * 4 : 0;
     const int64_t nC = extent_bytes(a.batch, a.M, a.N, a.ldc, a.sC, es);
     auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
-    const size_t need = up(nA) + up(nB) + up(nBias) + up(nS) + up(nC);
+    // stream-K workspace of the launches below (one fp32 128 x 256 slot and one flag per CTA,
+    // zero-filled once when allocated; every launch leaves the flags at zero)
+    const int64_t nSK = up(static_cast<int64_t>(sms) * (128 * 256 * 4 + 4));
+    const size_t need = nSK + up(nA) + up(nB) + up(nBias) + up(nS) + up(nC);
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_ws_mu);
@@ -814,9 +861,14 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
             return fail(GE_ERR_CUDA, "workspace cudaMalloc failed");
         }
         ws.bytes = need;
+        if (cudaMemsetAsync(ws.ptr, 0, nSK, st) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(GE_ERR_CUDA, "workspace memset failed");
+        }
     }
     char* base = static_cast<char*>(ws.ptr);
-    char* dA = base;
+    char* dSK = base;
+    char* dA = base + nSK;
     char* dB = dA + up(nA);
     char* dBias = dB + up(nB);
     char* dS = dBias + up(nBias);
@@ -871,6 +923,8 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
         if (!chk(cudaStreamWaitEvent(ps.cmp, ps.ev_in[blk], 0), "event")) return GE_ERR_CUDA;
         // the fused kernel on this block
         Args d = a;
+        d.o.workspace = dSK;
+        d.o.workspace_bytes = nSK;
         d.B = nB ? dB : nullptr;
         d.o.prologue_scale = nS ? reinterpret_cast<const float*>(dS) : nullptr;
         if (by_item) {
@@ -951,12 +1005,12 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0,
                        GE_EPI_NONE, opt);
     if (batch < 0 || M < 0 || N < 0 || K < 0 || num_sms <= 0) return fail(GE_ERR_INVALID_VALUE, "bad plan arguments");
-    if (a.o.tile_n != 0 && a.o.tile_n != 64 && a.o.tile_n != 128 && a.o.tile_n != 192 && a.o.tile_n != 256 &&
-        a.o.tile_n != 512)
-        return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 192, 256 or 512");
-    if (a.o.cta_group < 0 || a.o.cta_group > 2) return fail(GE_ERR_INVALID_VALUE, "cta_group must be 0, 1 or 2");
-    if (a.o.stream_k < 0 || a.o.stream_k > 2) return fail(GE_ERR_INVALID_VALUE, "stream_k must be 0, 1 or 2");
-    const Plan p = make_plan(a, num_sms, split_capacity());     // (nullptr without a device)
+    {
+        const ge_status so = validate_options(a);
+        if (so != GE_OK) return so;
+    }
+    // descriptive: assumes the caller will pass a workspace of *workspace_bytes when stream-K is planned
+    const Plan p = make_plan(a, num_sms, split_capacity(), true);     // (nullptr without a device)
     if (tile_m) *tile_m = 128 * p.cg * (p.mc ? 2 : 1);
     if (tile_n) *tile_n = p.bn;
     if (cta_group) *cta_group = p.cg;
@@ -970,10 +1024,15 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
 
 uint64_t ge_launch_count(void) { return g_launches.load(); }
 
+void ge_tensor_map_cache_stats(uint64_t* hits, uint64_t* misses) {
+    if (hits) *hits = g_map_hits.load();
+    if (misses) *misses = g_map_misses.load();
+}
+
 int32_t ge_debug_read(uint64_t* out, int32_t max_ctas) {
-    if (!g_dbg || !out) return 0;
-    const int n = std::min(max_ctas, g_dbg_ctas);
-    if (cudaMemcpy(out, g_dbg, sizeof(uint64_t) * 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    if (g_dbg_last < 0 || !g_dbg[g_dbg_last] || !out) return 0;
+    const int n = std::min(max_ctas, g_dbg_ctas[g_dbg_last]);
+    if (cudaMemcpy(out, g_dbg[g_dbg_last], sizeof(uint64_t) * 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }

@@ -112,8 +112,10 @@ struct Params {
     int splits;
     // diagnostics (GE_DEBUG_STATS): per-CTA blocked-cycle counters, or nullptr
     unsigned long long* dbg;
-    int dbg_noload;                 // dev experiment only: stop issuing TMA after the ring is full once
-    int dbg_flags;                  // dev experiments only (GE_DEBUG_FLAGS): 1 skip epilogue, 8 no epilogue math, 16 no stores
+    // timing experiments, read only by the diagnostics build (GE_DBG = 1; the production kernels
+    // compile these branches out, so no environment variable can change their results)
+    int dbg_noload;                 // GE_DEBUG_NOLOAD: stop issuing TMA after the ring is full once
+    int dbg_flags;                  // GE_DEBUG_FLAGS: 1 skip epilogue, 8 no epilogue math, 16 no stores
 };
 
 // Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
@@ -252,8 +254,10 @@ struct WorkSeq {
     __device__ __forceinline__ bool has_units(int c) const { return range_begin(c + 1) > range_begin(c); }
 };
 
-// Activation at the root of the pointwise epilogue, fp32, IEEE
-// library functions (no fast math, DESIGN.md R-C7).  ReLU: y = v > 0 ? v : +0 (DESIGN.md R-C5).
+// Activation at the root of the pointwise epilogue, fp32 (DESIGN.md
+// R-C7): ReLU y = v > 0 ? v : +0 (R-C5) and Tanh (tanhf) are IEEE/library-accurate; Sigmoid uses
+// the fast __expf (ex2.approx) and the RN reciprocal, relative error ~1e-7, far below the
+// fp16 output rounding the bound allows.
 __device__ __forceinline__ void activate(float* f, int n, int act) {
     if (act == ACT_RELU) {
 #pragma unroll
@@ -397,7 +401,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     const int k0 = (second ? kb - p.num_k_blocks1 : kb) * kBK;
                     uint8_t* sa = smem_a + s * C_::kAStage;
                     uint8_t* sb = smem_b + s * C_::kBStage;
-                    if (p.dbg_noload && (wi != 0 || kb >= S)) {
+                    if (GE_DBG && p.dbg_noload && (wi != 0 || kb >= S)) {
                         // timing experiment (GE_DEBUG_NOLOAD): operands stay resident, results invalid
                         if (CG == 1 || PRO || leader) ptx::mbar_arrive(&full_bar[s]);
                         if (++s == S) { s = 0; phase ^= 1; }
@@ -590,7 +594,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         uint8_t* stage_c = smem_c + e_idx * (NBUF * STG);
         const uint64_t pol_c = ptx::l2_policy(p.hint_c);
         const bool epi_fast = (C_::kBiasF32 || (GE_EPI_FAST512 && p.bias_sign > 0.0f)) && !p.literal && p.act == ACT_RELU &&
-                              p.bias_mode == BIAS_ROW && !p.dbg_flags;
+                              p.bias_mode == BIAS_ROW && !(GE_DBG && p.dbg_flags);
         int buf = 0;
         for (int jj = 0; jj < work.count(); ++jj) {
             const int it = work.epi_index(jj);
@@ -964,7 +968,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
             };
 
-            if (p.dbg_flags & 1) {          // timing experiment: release without draining
+            if (GE_DBG && (p.dbg_flags & 1)) {   // timing experiment (debug build only): release without draining
 #pragma unroll
                 for (int h = 0; h < NH; ++h) release(h);
                 continue;
@@ -1033,13 +1037,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (j == CPH - 1) release(h);
                         if (pc.kind == PIECE_OWNER) add_partials(c, v);
                         uint32_t w[NWORD];
-                        if (p.dbg_flags & 8) {      // timing experiment: no epilogue math
+                        if (GE_DBG && (p.dbg_flags & 8)) {   // timing experiment (debug build only): no epilogue math
 #pragma unroll
                             for (int e = 0; e < NWORD; ++e) w[e] = v[e];
                         } else {
                             compute(c, v, w);
                         }
-                        if (!(p.dbg_flags & 16)) store(c, w);   // 16: timing experiment, no stores
+                        if (!(GE_DBG && (p.dbg_flags & 16))) store(c, w);   // 16: timing experiment (debug build), no stores
                         else if (p.dbg && w[0] == 0x12345678u && w[NWORD - 1] == 0x9abcdef0u) p.dbg[0] = 1;
                     }
                 }

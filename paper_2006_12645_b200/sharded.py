@@ -5,9 +5,15 @@ single-GPU).  So the data path shards with NO collective:
 
 * batched problems split the batch into contiguous blocks, rank r owning items
   [r*B/P, (r+1)*B/P) (remainders spread over the first ranks);
-* a single large GEMM splits M into row blocks cut at multiples of the 256-row tile, so every rank
-  runs exactly the tiles the 1-GPU launch would (bitwise-identical results); A is sliced by rows,
-  B and bias are replicated, and each rank's C rows are contiguous in row-major C.
+* a single large GEMM splits M into row blocks cut at multiples of the 256-row tile; A is sliced by
+  rows, B and a row bias are replicated (a column or full bias is sliced with A's rows), and each
+  rank's C rows are contiguous in row-major C.
+
+Per rank the fused kernel computes exactly the definition on its slice, so shards always agree
+with the 1-GPU result within the north_star bound.  They agree BITWISE when every rank's launch
+runs the same tile configuration with no split or stream-K reduction (a smaller per-rank problem
+can change the planner's choice and with it the fp32 summation order, DESIGN.md R-C13): pass
+``stream_k=1`` and an explicit ``tile_n``/``cta_group`` to pin it.
 
 A collective appears only when the caller asks for the full output on every rank
 (``gather=True``): one NCCL all-gather of the row/batch blocks over NVLink/NVSwitch, off the hot
@@ -75,19 +81,28 @@ def sharded_gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Option
     lo, hi = shard_range(total, rank, world)
     if not presliced:
         A, B = A[lo:hi], B[lo:hi]
-        if bias is not None and bias.dim() == 2:
-            bias = bias[lo:hi]
+        bias = _slice_bias_items(bias, kw.get("bias_mode", "row"), lo, hi)
     fn = compute or gemm_epilogue_batched
-    C = fn(A, B, bias, **kw) if hi > lo else torch.empty((0, A.shape[1], B.shape[2]), dtype=torch.float16,
-                                                         device=A.device)
+    C = fn(A, B, bias, **kw) if hi > lo else torch.empty((0, A.shape[1], B.shape[2]),
+                                                         dtype=kw.get("out_dtype", torch.float16), device=A.device)
     return gather_rows(C, total) if gather else C
+
+
+def _slice_bias_items(bias, bias_mode, lo, hi):
+    """Per-item biases are sliced to the rank's items; a bias shared by every item is passed as is:
+    row/col: (b, L) per item vs (L,) shared; full: (b, M, ld) per item vs (M, ld) shared."""
+    if bias is None:
+        return None
+    per_item = bias.dim() == (3 if bias_mode == "full" else 2)
+    return bias[lo:hi] if per_item else bias
 
 
 def sharded_gemm_epilogue_rows(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None, *,
                                gather: bool = False, compute=None, **kw) -> torch.Tensor:
     """Row-block (M) shard of one GEMM: rank r computes rows shard_range(M, r, P, 256) of C.
-    A is the full (M, K) operand or the rank's row block (``presliced=True``); B, bias replicated
-    (a COL bias is sliced with A)."""
+    A is the full (M, K) operand or the rank's row block (``presliced=True``, then a COL/FULL bias
+    must be the rank's rows too); B and a ROW bias are replicated, a COL (M,) or FULL (M, ld) bias
+    is sliced with A's rows."""
     from . import gemm_epilogue
     presliced = kw.pop("presliced", False)
     M = kw.pop("total_rows", A.shape[0])
@@ -95,8 +110,9 @@ def sharded_gemm_epilogue_rows(A: torch.Tensor, B: torch.Tensor, bias: Optional[
     lo, hi = shard_range(M, rank, world, ROW_QUANTUM)
     if not presliced:
         A = A[lo:hi]
-        if bias is not None and kw.get("bias_mode") == "col":
-            bias = bias[lo:hi]
+        if bias is not None and kw.get("bias_mode", "row") in ("col", "full"):
+            bias = bias[lo:hi]          # bias[i] / bias[i, :] follow the rows of A
     fn = compute or gemm_epilogue
-    C = fn(A, B, bias, **kw) if hi > lo else torch.empty((0, B.shape[1]), dtype=torch.float16, device=A.device)
+    C = fn(A, B, bias, **kw) if hi > lo else torch.empty((0, B.shape[1]), dtype=kw.get("out_dtype", torch.float16),
+                                                         device=A.device)
     return gather_rows(C, M, ROW_QUANTUM) if gather else C

@@ -32,14 +32,14 @@ def lib(ge):
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(?:ge_status|uint64_t|int32_t|const char\*)\s+(\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(?:ge_status|uint64_t|int32_t|void|const char\*)\s+(\w+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(lib):
     names = declared_functions()
     assert {"gemm_epilogue", "gemm_epilogue_batched", "gemm_epilogue_host", "ge_validate", "ge_status_string",
             "ge_last_error_detail", "ge_plan", "ge_launch_count", "ge_version",
-            "ge_release_workspace", "ge_debug_read"} <= set(names)
+            "ge_release_workspace", "ge_debug_read", "ge_tensor_map_cache_stats"} <= set(names)
     for n in names:
         assert hasattr(lib, n), n
 
@@ -198,3 +198,44 @@ def test_binding_layout_detection(ge):
     assert ge.layout_of(Y) == (0, 48)
     with pytest.raises(ValueError):
         ge.layout_of(torch.zeros((8, 8, 2), dtype=torch.float16)[:, :, 0])
+
+
+def test_plan_rejects_what_launch_rejects(ge):
+    """ge_plan runs the launch entry points' option checks: invalid combinations are
+    GE_ERR_INVALID_VALUE instead of an arbitrary plan."""
+    for kw in (dict(multicast=2, tile_n=64), dict(multicast=2, prologue="scale_k"), dict(multicast=3),
+               dict(tile_n=192, cta_group=2, layouts="rr"), dict(tile_n=512, cta_group=1), dict(cta_group=3),
+               dict(stream_k=3)):
+        with pytest.raises(ge.GEError) as e:
+            ge.plan(1024, 1024, 1024, **kw)
+        assert e.value.status == ge.Status.INVALID_VALUE, kw
+    assert ge.plan(1024, 1024, 1024, tile_n=192, cta_group=2, layouts="rc")["tile_n"] == 192
+
+
+def test_binding_rejects_bad_tensors(ge):
+    """The binding checks what the C ABI cannot see (dtype, shape, device) before any launch
+    (ADVICE r1): wrong dtypes, an output of the wrong shape, a bias of the wrong length for its
+    mode, a short or non-fp32 scale, and device tensors for the host entry all raise ValueError."""
+    h = lambda *s: torch.zeros(s, dtype=torch.float16)
+    A, B, bias = h(64, 32), h(32, 48), h(48)
+    bad = [
+        dict(A=A.float()), dict(B=B.to(torch.bfloat16)), dict(bias=bias.float()), dict(bias=h(47)),
+        dict(bias=h(64), bias_mode="row"), dict(bias=h(48), bias_mode="col"), dict(bias=h(64, 40), bias_mode="full"),
+        dict(out=torch.zeros((64, 47), dtype=torch.float16)), dict(out=torch.zeros((64, 48), dtype=torch.bfloat16)),
+        dict(prologue="scale_k", scale=torch.ones(31)), dict(prologue="scale_k", scale=torch.ones(32).double()),
+        dict(prologue="scale_k", scale=None),
+    ]
+    for kw in bad:
+        args = dict(A=A, B=B, bias=bias)
+        args.update(kw)
+        with pytest.raises(ValueError):
+            ge.gemm_epilogue_host(args.pop("A"), args.pop("B"), args.pop("bias"), **args)
+    with pytest.raises(ValueError):                   # host tensors on the device entry point
+        ge.gemm_epilogue(A, B, bias)
+    with pytest.raises(ValueError):
+        ge.gemm_epilogue_batched(h(2, 64, 32), h(2, 32, 48), h(3, 48))      # per-item bias of the wrong batch
+
+
+def test_tensor_map_cache_stats_exported(ge):
+    s = ge.tensor_map_cache_stats()
+    assert set(s) == {"hits", "misses"} and s["hits"] >= 0 and s["misses"] >= 0

@@ -152,7 +152,10 @@ def test_batched_64x2048():
     B = (torch.rand(batch, K, N, generator=g, device="cuda") * 2 - 1).half()
     bias = (torch.rand(batch, N, generator=g, device="cuda") * 2 - 1).half()
     C = ge.gemm_epilogue_batched(A, B, bias)
+    from paper_2006_12645_b200 import sharded
+    Cs = sharded.sharded_gemm_epilogue_batched(A, B, bias, total_batch=batch)   # bench's N > 1 path at world 1
     torch.cuda.synchronize()
+    assert torch.equal(Cs, C)
     rows, cols = sample_idx(M, 64, 3), sample_idx(N, 64, 4)
     for b in (0, 17, 63):
         single = ge.gemm_epilogue(A[b], B[b], bias[b])

@@ -632,3 +632,26 @@ def test_fast_epilogue_matches_general(tile_n, cg, out_dtype, N):
     got = fast.float().cpu().numpy().astype(np.float64)
     out, mag = oracle_run(prob, "rc")
     check_bound(got, out, mag, "fast epilogue")
+
+
+# ------------------------------------------------------------------ multi-GPU sharding, CUDA path (world 1)
+@pytest.mark.parametrize("bias_mode", ["row", "col", "full"])
+def test_sharded_world1_is_the_batched_call(bias_mode):
+    """sharded.py on the CUDA path (no process group: world 1) is the plain batched / single call,
+    bitwise, for per-item and shared biases of every mode."""
+    from paper_2006_12645_b200 import sharded
+    batch, M, N, K = 6, 300, 264, 200
+    g = torch.Generator(device="cuda").manual_seed(90)
+    U = lambda *s: (torch.rand(*s, generator=g, device="cuda") * 2 - 1).half()
+    A, B = U(batch, M, K), U(batch, K, N).transpose(1, 2).contiguous().transpose(1, 2)
+    L = {"row": (N,), "col": (M,), "full": (M, N + 8)}[bias_mode]
+    for bias in (U(batch, *L), U(*L)):
+        got = sharded.sharded_gemm_epilogue_batched(A, B, bias, bias_mode=bias_mode)
+        want = ge.gemm_epilogue_batched(A, B, bias, bias_mode=bias_mode)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
+    b2 = U(*L)
+    got = sharded.sharded_gemm_epilogue_rows(A[0], B[0], b2, bias_mode=bias_mode)
+    want = ge.gemm_epilogue(A[0], B[0], b2, bias_mode=bias_mode)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
