@@ -37,7 +37,7 @@
  * aligned and lda*2, ldb*2 (and batch strides *2) multiples of 16 bytes, else
  * GE_ERR_MISALIGNED.  C, bias and scale have no alignment requirement: a C whose base or
  * ldc is not 16-byte compatible is written by a st.global epilogue instead of TMA stores.
- * Aliasing: C must not overlap A, B, bias or scale (`__restrict__`), else
+ * Aliasing: C must not overlap A, B, bias, scale or the prologue tile (`__restrict__`), else
  * GE_ERR_ALIASING.
  * Degenerate sizes: M == 0 or N == 0 (or batch == 0) is a no-op returning GE_OK.
  * K == 0 gives C = op(bias) (DESIGN.md R-C9).
@@ -87,7 +87,11 @@ typedef enum {
 typedef enum {
     GE_PRO_NONE = 0,
     GE_PRO_SCALE_K = 1,     /* a'(i,k) = fp16_rne(s[k] * a(i,k)), s = prologue_scale, fp32, length K */
-    GE_PRO_RELU = 2         /* a'(i,k) = max(a(i,k), +0)  (Listing 5)          */
+    GE_PRO_RELU = 2,        /* a'(i,k) = max(a(i,k), +0)  (Listing 5)          */
+    GE_PRO_HADAMARD = 3     /* a'(i,k) = fp16_rne(s(i,k) * a(i,k)): a full-tile elementwise scale, a
+                               second input dataspace of the prologue's compound op (
+                               DESIGN.md R-C18).  S = prologue_tile, fp16, M x K in A's layout
+                               (row-major: s(i,k) = S[i*lds + k]; col-major: S[k*lds + i]). */
 } ge_prologue_op;
 
 typedef struct {
@@ -115,7 +119,12 @@ typedef struct {
                                        along M (512 x tile_n tiles) whose B tiles are loaded once and
                                        TMA-multicast to both pairs (a third less L2->SM traffic per flop;
                                        needs no prologue and stream_k != 2; data-parallel tiles only) */
-} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0} */
+    const void* prologue_tile;      /* HADAMARD only: S (device pointer; host pointer for *_host), fp16,
+                                       M x K in A's layout; 16-byte aligned, ld_prologue_tile * 2 and
+                                       stride_prologue_tile * 2 multiples of 16 (else GE_ERR_MISALIGNED) */
+    int64_t ld_prologue_tile;       /* leading dimension of S in elements (0 = packed: K row-major, M col-major) */
+    int64_t stride_prologue_tile;   /* batched: element stride between items' S (0 = one S shared by all) */
+} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0, NULL, 0, 0} */
 
 typedef enum {
     GE_OK = 0,
@@ -234,10 +243,11 @@ uint64_t ge_launch_count(void);
 void ge_tensor_map_cache_stats(uint64_t* hits, uint64_t* misses);
 
 /*
- * Diagnostics: when the process runs with GE_DEBUG_STATS=1, every launch records per-CTA
- * counters (16 x uint64 per CTA: total cycles, producer cycles blocked on free stages, MMA
- * cycles blocked on loaded stages, MMA cycles blocked on a drained accumulator, epilogue
- * cycles blocked on a full accumulator, epilogue phase timings, reserved).  Copies the last launch's counters of up to
+ * Diagnostics: when the process runs with GE_DEBUG_STATS=1 (diagnostics build), every launch
+ * records per-CTA counters (20 x uint64 per CTA: total cycles, producer cycles blocked on free
+ * stages, MMA cycles blocked on loaded stages, MMA cycles blocked on a drained accumulator,
+ * epilogue cycles blocked on a full accumulator, epilogue phase timings, and %globaltimer
+ * stamps (ns) of kernel entry, end of setup, end of the epilogue and exit).  Copies the last launch's counters of up to
  * max_ctas CTAs into out (synchronizing) and returns how many were copied (0 when disabled).
  */
 int32_t ge_debug_read(uint64_t* out, int32_t max_ctas);

@@ -32,7 +32,7 @@ _lib = None
 
 LAYOUT = {"row": 0, "col": 1}
 BIAS_MODE = {None: -1, "none": -1, "row": 0, "col": 1, "full": 2}
-PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
+PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2, "hadamard": 3}
 ACT = {None: 0, "none": 0, "relu": 1, "sigmoid": 2, "tanh": 3}
 
 
@@ -61,7 +61,7 @@ def _load():
         lib.oracle_f16_decode_array.argtypes = [P, P, I64]
         lib.oracle_f16_encode_array.argtypes = [P, P, I64]
         lib.oracle_gemm_epilogue.restype = I
-        lib.oracle_gemm_epilogue.argtypes = [I64, I64, I64, I, I, P, I64, P, I64, P, I, I, I64, I, I, P, I,
+        lib.oracle_gemm_epilogue.argtypes = [I64, I64, I64, I, I, P, I64, P, I64, P, I, I, I64, I, I, P, P, I64, I,
                                              P, I64, P, I64, P, P, I]
         lib.oracle_gemm2_epilogue.restype = I
         lib.oracle_gemm2_epilogue.argtypes = [I64, I64, I64, I64, I, I, P, I64, P, I64, P, I64, P, I64, P, I, I, I64,
@@ -111,14 +111,15 @@ def gemm_epilogue(A, B, M: int, N: int, K: int, *, layoutA: str = "row", layoutB
                   lda: Optional[int] = None, ldb: Optional[int] = None,
                   bias=None, bias_mode: Optional[str] = "row", ldbias: int = 0,
                   relu: bool = True, act: Optional[str] = "default", bias_sub: bool = False,
-                  prologue: Optional[str] = None, scale=None,
+                  prologue: Optional[str] = None, scale=None, lds: Optional[int] = None,
                   literal_round: bool = False,
                   rows: Optional[Sequence[int]] = None, cols: Optional[Sequence[int]] = None,
                   nthreads: Optional[int] = None):
     """Evaluate the oracle.  Returns (out, mag) as fp64 arrays of shape (len(rows), len(cols))
     (full M x N when rows/cols are None).  A and B are fp16 storage arrays (flat or 2-D)
     read through the layout index formulas with leading dimensions lda/ldb
-    (default: packed).  ``bias=None`` means no bias term.  The activation is ``act`` (None, "relu",
+    (default: packed).  ``bias=None`` means no bias term.  prologue "hadamard": ``scale`` is the fp16
+    storage of S (M x K in A's layout, leading dimension ``lds``, default packed).  The activation is ``act`` (None, "relu",
     "sigmoid", "tanh"); by default ReLU if ``relu`` else identity.  ``bias_sub`` subtracts the bias.
     """
     lib = _load()
@@ -132,6 +133,11 @@ def gemm_epilogue(A, B, M: int, N: int, K: int, *, layoutA: str = "row", layoutB
     bb = np.ascontiguousarray(_bits(bias)).reshape(-1) if bias is not None else None
     pro = PROLOGUE[prologue]
     sc = None
+    st = None
+    if pro == 3:
+        st = np.ascontiguousarray(_bits(scale)).reshape(-1)
+        if lds is None:
+            lds = K if layoutA == "row" else M
     if pro == 1:
         sc = np.ascontiguousarray(np.asarray(scale.cpu().numpy() if hasattr(scale, "cpu") else scale,
                                              dtype=np.float32)).reshape(-1)
@@ -146,7 +152,8 @@ def gemm_epilogue(A, B, M: int, N: int, K: int, *, layoutA: str = "row", layoutB
         M, N, K, LAYOUT[layoutA], LAYOUT[layoutB],
         a.ctypes.data, lda, b.ctypes.data, ldb,
         bb.ctypes.data if bb is not None else None, bm, -1 if bias_sub else 1, ldbias, act_code,
-        pro, sc.ctypes.data if sc is not None else None, int(bool(literal_round)),
+        pro, sc.ctypes.data if sc is not None else None, st.ctypes.data if st is not None else None,
+        int(lds or 0), int(bool(literal_round)),
         r.ctypes.data if r is not None else None, 0 if r is None else r.size,
         c.ctypes.data if c is not None else None, 0 if c is None else c.size,
         out.ctypes.data, mag.ctypes.data, int(nthreads or default_threads()))

@@ -16,9 +16,13 @@
  *   bias, then ReLU, Sigmoid or Tanh at the root.
  *   Listing 5 (Sec. VII-C "Pointwise Operations in Prologue"):
  *       C[i,j] = sum_k relu(A[i,k]) * B[k,j]
- *   plus the SCALE_K prologue reading of DESIGN.md (R-C12): a'(i,k) = s_k * a(i,k).
+ *   plus the SCALE_K prologue reading of DESIGN.md (R-C12): a'(i,k) = s_k * a(i,k), and the
+ *   full-tile Hadamard prologue (DESIGN.md R-C18; "the compound operation in statement S1 could have
+ *   multiple input dataspaces"): a'(i,k) = s(i,k) * a(i,k), S an M x K fp16
+ *   dataspace stored in A's layout.
  *
- *   a'(i,k)  = a(i,k) | s_k * a(i,k) | max(a(i,k), 0)        (prologue NONE|SCALE_K|RELU)
+ *   a'(i,k)  = a(i,k) | s_k * a(i,k) | max(a(i,k), 0) | s(i,k) * a(i,k)
+ *                                                       (prologue NONE|SCALE_K|RELU|HADAMARD)
  *   pre(i,j) = sum_{k<K} a'(i,k) * b(k,j) +- beta(i,j)        (beta = 0|bias[j]|bias[i]|bias[i,j])
  *   out(i,j) = act(pre): identity | relu (pre > 0 ? pre : +0) | sigmoid 1/(1+e^-pre) | tanh(pre)
  *   mag(i,j) = sum_{k<K} |a'(i,k) * b(k,j)|                    (scale of the rounding error)
@@ -97,7 +101,7 @@ uint16_t oracle_f64_to_f16_rne(double x) {
 /* ------------------------------------------------------------ definitions */
 enum { OR_ROW = 0, OR_COL = 1 };
 enum { OR_BIAS_NONE = -1, OR_BIAS_ROW = 0, OR_BIAS_COL = 1, OR_BIAS_FULL = 2 };
-enum { OR_PRO_NONE = 0, OR_PRO_SCALE_K = 1, OR_PRO_RELU = 2 };
+enum { OR_PRO_NONE = 0, OR_PRO_SCALE_K = 1, OR_PRO_RELU = 2, OR_PRO_HADAMARD = 3 };
 
 typedef struct {
     int64_t M, N, K;
@@ -108,6 +112,7 @@ typedef struct {
     int act;                /* 0 identity, 1 relu, 2 sigmoid, 3 tanh */
     int bias_sign;          /* +1 add, -1 subtract */
     int prologue; const float *scale;
+    const uint16_t *S; int64_t lds;     /* HADAMARD: s(i,k), A's layout */
     int literal_round;      /* DESIGN.md R-C3 paper-literal variant: relu(f16(f16(acc)+bias)) */
     /* the evaluated rows I and columns J (the output is out[r*nJ + c] for i=I[r], j=J[c]) */
     const int64_t *I; int64_t nI;
@@ -131,11 +136,18 @@ static double b_elem(const job_t *T, int64_t k, int64_t j) {
     uint16_t h = (T->layoutB == OR_ROW) ? T->B[k * T->ldb + j] : T->B[j * T->ldb + k];
     return oracle_f16_to_f64(h);
 }
-/* prologue a'(i,k): PAPER.md:1201-1206 (ReLU) and DESIGN.md R-C12 (SCALE_K) */
+/* s(i,k) of the Hadamard prologue, read through A's layout formula */
+static double s_elem(const job_t *T, int64_t i, int64_t k) {
+    uint16_t h = (T->layoutA == OR_ROW) ? T->S[i * T->lds + k] : T->S[k * T->lds + i];
+    return oracle_f16_to_f64(h);
+}
+/* prologue a'(i,k): PAPER.md:1201-1206 (ReLU), DESIGN.md R-C12 (SCALE_K) and R-C18 (HADAMARD,
+ * PAPER.md:1222-1224) */
 static double a_prime(const job_t *T, int64_t i, int64_t k) {
     double a = a_elem(T, i, k);
     if (T->prologue == OR_PRO_SCALE_K) return (double)T->scale[k] * a;
     if (T->prologue == OR_PRO_RELU) return a > 0.0 ? a : 0.0;
+    if (T->prologue == OR_PRO_HADAMARD) return s_elem(T, i, k) * a;
     return a;
 }
 /* beta(i,j): DESIGN.md R-C2 (ROW default, COL, FULL = PAPER.md:363 literal) */
@@ -218,18 +230,21 @@ static int run_threads(job_t *base, void *(*fn)(void *)) {
  * I == NULL means all M rows (nI ignored), J == NULL all N columns.
  * out[r*nJ + c] is element (I[r], J[c]).  Returns 0, or <0 on bad arguments.
  * bias_mode: -1 none, 0 ROW bias[j], 1 COL bias[i], 2 FULL bias[i*ldbias+j]; bias_sign +1/-1.
- * act: 0 identity, 1 relu, 2 sigmoid, 3 tanh.  prologue: 0 none, 1 SCALE_K (scale[k], fp32), 2 RELU.
+ * act: 0 identity, 1 relu, 2 sigmoid, 3 tanh.  prologue: 0 none, 1 SCALE_K (scale[k], fp32), 2 RELU,
+ * 3 HADAMARD (S: fp16 M x K in A's layout with leading dimension lds).
  */
 int oracle_gemm_epilogue(int64_t M, int64_t N, int64_t K, int layoutA, int layoutB,
                          const uint16_t *A, int64_t lda, const uint16_t *B, int64_t ldb,
                          const uint16_t *bias, int bias_mode, int bias_sign, int64_t ldbias, int act,
-                         int prologue, const float *scale, int literal_round,
+                         int prologue, const float *scale, const uint16_t *S, int64_t lds, int literal_round,
                          const int64_t *I, int64_t nI, const int64_t *J, int64_t nJ,
                          double *out, double *mag, int nthreads) {
     if (M < 0 || N < 0 || K < 0) return -1;
     if (act < 0 || act > 3 || (bias_sign != 1 && bias_sign != -1)) return -1;
     if (bias_mode != OR_BIAS_NONE && !bias) return -1;
     if (prologue == OR_PRO_SCALE_K && !scale) return -1;
+    if (prologue == OR_PRO_HADAMARD && K > 0 && !S) return -1;
+    if (prologue < OR_PRO_NONE || prologue > OR_PRO_HADAMARD) return -1;
     job_t T;
     memset(&T, 0, sizeof T);
     T.M = M; T.N = N; T.K = K;
@@ -237,6 +252,7 @@ int oracle_gemm_epilogue(int64_t M, int64_t N, int64_t K, int layoutA, int layou
     T.A = A; T.lda = lda; T.B = B; T.ldb = ldb;
     T.bias = bias; T.bias_mode = bias_mode; T.ldbias = ldbias;
     T.act = act; T.bias_sign = bias_sign; T.prologue = prologue; T.scale = scale;
+    T.S = S; T.lds = lds;
     T.literal_round = literal_round;
     T.I = I; T.nI = I ? nI : M;
     T.J = J; T.nJ = J ? nJ : N;
@@ -287,10 +303,10 @@ int oracle_gemm2_epilogue(int64_t M, int64_t N, int64_t K1, int64_t K2, int layo
     int rc = (c && cm && r && rm) ? 0 : -3;
     if (rc == 0)
         rc = oracle_gemm_epilogue(M, N, K1, layoutA, layoutB, A, lda, B, ldb, NULL, OR_BIAS_NONE, 1, 0, 0,
-                                  OR_PRO_NONE, NULL, 0, I, nI, J, nJ, c, cm, nthreads);
+                                  OR_PRO_NONE, NULL, NULL, 0, 0, I, nI, J, nJ, c, cm, nthreads);
     if (rc == 0)
         rc = oracle_gemm_epilogue(M, N, K2, layoutA, layoutB, P, ldp, Q, ldq, NULL, OR_BIAS_NONE, 1, 0, 0,
-                                  OR_PRO_NONE, NULL, 0, I, nI, J, nJ, r, rm, nthreads);
+                                  OR_PRO_NONE, NULL, NULL, 0, 0, I, nI, J, nJ, r, rm, nthreads);
     if (rc == 0) {
         job_t T;
         memset(&T, 0, sizeof T);

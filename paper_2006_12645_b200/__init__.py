@@ -45,14 +45,16 @@ EPI = {"none": 0, "bias": 1, "relu": 2, "bias_relu": 3, "sigmoid": 4, "bias_sigm
        "sub_bias": 17, "sub_bias_relu": 19, "sub_bias_sigmoid": 21, "sub_bias_tanh": 25}
 EPI_F16_INTERMEDIATE = 32
 BIAS_MODE = {"row": 0, "col": 1, "full": 2}
-PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2}
+PROLOGUE = {None: 0, "none": 0, "scale_k": 1, "relu": 2, "hadamard": 3}
 
 
 class GEOptions(ctypes.Structure):
     _fields_ = [("bias_mode", ctypes.c_int32), ("ldbias", ctypes.c_int64), ("prologue", ctypes.c_int32),
                 ("prologue_scale", ctypes.c_void_p), ("out_dtype", ctypes.c_int32), ("tile_n", ctypes.c_int32),
                 ("cta_group", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace", ctypes.c_void_p),
-                ("workspace_bytes", ctypes.c_int64), ("multicast", ctypes.c_int32)]
+                ("workspace_bytes", ctypes.c_int64), ("multicast", ctypes.c_int32),
+                ("prologue_tile", ctypes.c_void_p), ("ld_prologue_tile", ctypes.c_int64),
+                ("stride_prologue_tile", ctypes.c_int64)]
 
 
 class GEError(RuntimeError):
@@ -155,11 +157,13 @@ def clear_workspaces():
 _opt_cache = {}
 
 
-def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, stream_k=0, ws=None, multicast=0):
-    """ge_options for these arguments; reused across calls with the same ones (per-call host cost)."""
+def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, stream_k=0, ws=None, multicast=0,
+             tile=None):
+    """ge_options for these arguments; reused across calls with the same ones (per-call host cost).
+    tile: (ptr, ld, batch stride) of the Hadamard prologue operand S."""
     key = (bias_mode, ldbias, prologue, scale.data_ptr() if scale is not None else 0, out_dtype, tile_n,
            cta_group, stream_k, ws.data_ptr() if ws is not None else 0, ws.numel() if ws is not None else 0,
-           multicast)
+           multicast, tile)
     o = _opt_cache.get(key)
     if o is not None:
         return o
@@ -170,7 +174,9 @@ def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, s
     o.bias_mode = BIAS_MODE[bias_mode]
     o.ldbias = int(ldbias or 0)
     o.prologue = PROLOGUE[prologue]
-    o.prologue_scale = scale.data_ptr() if scale is not None else None
+    o.prologue_scale = scale.data_ptr() if (scale is not None and prologue == "scale_k") else None
+    if tile is not None:
+        o.prologue_tile, o.ld_prologue_tile, o.stride_prologue_tile = tile
     o.out_dtype = 1 if out_dtype == torch.float32 else 0
     o.tile_n = int(tile_n)
     o.cta_group = int(cta_group)
@@ -179,6 +185,29 @@ def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, s
         _opt_cache.clear()
     _opt_cache[key] = o
     return o
+
+
+def _prologue_tile(prologue, scale, A, batch=None):
+    """(ptr, ld, batch stride) of the Hadamard operand S (prologue="hadamard", passed as `scale`):
+    fp16, the logical shape of A ((M, K), or (batch, M, K) / a shared (M, K) for batched calls),
+    stored in A's layout (DESIGN.md R-C18)."""
+    if prologue != "hadamard":
+        return None
+    if scale is None:
+        raise ValueError("prologue 'hadamard' needs scale = the (M, K) fp16 tile S")
+    if scale.dtype != torch.float16:
+        raise ValueError(f"the Hadamard tile must be float16, got {scale.dtype}")
+    if scale.shape[-2:] != A.shape[-2:] or scale.dim() not in ((2, 3) if batch is not None else (2,)):
+        raise ValueError(f"the Hadamard tile must have A's shape {tuple(A.shape[-2:])}, got {tuple(scale.shape)}")
+    if scale.dim() == 3 and scale.shape[0] != batch:
+        raise ValueError("per-item Hadamard tiles need one per batch item")
+    if scale.device != A.device:
+        raise ValueError("the Hadamard tile must be on A's device")
+    ls, lds = layout_of(scale)
+    la, _ = layout_of(A)
+    if ls != la:
+        raise ValueError("the Hadamard tile must have A's layout (row- or column-major)")
+    return (scale.data_ptr(), lds, scale.stride(0) if scale.dim() == 3 else 0)
 
 
 def _stream(stream, device_index: Optional[int] = None) -> int:
@@ -278,7 +307,8 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     (M,) for "col", (M, ldbias>=N) row-major for "full".  op in {"none", "bias", "relu", "bias_relu",
     "sigmoid", "bias_sigmoid", "tanh", "bias_tanh", "sub_bias", "sub_bias_relu", "sub_bias_sigmoid",
     "sub_bias_tanh"}, each optionally prefixed "literal_" for the paper-literal fp16 rounding of the
-    intermediate (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32) or "relu".
+    intermediate (default: bias_relu if bias is given else relu).  prologue "scale_k" (scale: (K,) fp32),
+    "relu", or "hadamard" (scale: the (M, K) fp16 tile S in A's layout, a'(i,k) = fp16(S[i,k] * A[i,k])).
     Returns C (M, N) row-major in out_dtype (fp16 or fp32), asynchronously on the current stream.
     """
     lib = load_library()
@@ -290,7 +320,9 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
         raise ValueError(f"inner dimensions differ: A is {tuple(A.shape)}, B is {tuple(B.shape)}")
     if prologue == "scale_k" and scale is None:
         raise ValueError("prologue 'scale_k' needs scale")
-    _check_tensors(M, N, K, ops=(("A", A), ("B", B)), bias=bias, bias_mode=bias_mode, scale=scale, out=out)
+    tile = _prologue_tile(prologue, scale, A)
+    _check_tensors(M, N, K, ops=(("A", A), ("B", B)), bias=bias, bias_mode=bias_mode,
+                   scale=scale if prologue == "scale_k" else None, out=out)
     la, lda = layout_of(A)
     lb, ldb = layout_of(B)
     if out is None:
@@ -300,7 +332,7 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     ldbias, _ = _bias_ld(bias, bias_mode)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile)
     st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
                            bias.data_ptr() if bias is not None else None, out.data_ptr(), max(out.stride(0), N, 1),
                            _op(op, bias), ctypes.byref(o), sh)
@@ -370,12 +402,14 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
     lib = load_library()
     if prologue == "scale_k" and scale is None:
         raise ValueError("prologue 'scale_k' needs scale")
-    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A, B, bias, bias_mode, out, scale)
+    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(
+        A, B, bias, bias_mode, out, scale if prologue == "scale_k" else None)
+    tile = _prologue_tile(prologue, scale, A, batch)
     if out is None:
         out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile)
     st = lib.gemm_epilogue_batched(batch, M, N, K, la, lb, A.data_ptr(), lda, sA, B.data_ptr(), ldb, sB,
                                    bias.data_ptr() if bias is not None else None, sbias, out.data_ptr(),
                                    max(out.stride(1), N, 1), out.stride(0), _op(op, bias), ctypes.byref(o), sh)
@@ -396,13 +430,15 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
     if prologue == "scale_k" and scale is None:
         raise ValueError("prologue 'scale_k' needs scale")
     out3 = None if out is None else (out if out.dim() == 3 else out.unsqueeze(0))
-    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(A3, B3, bias, bias_mode, out3, scale,
-                                                                            host=True)
+    batch, M, N, K, la, lda, sA, lb, ldb, sB, ldbias, sbias = _batched_args(
+        A3, B3, bias, bias_mode, out3, scale if prologue == "scale_k" else None, host=True)
+    tile = _prologue_tile(prologue, scale, A3, batch)
     if out is None:
         out = torch.empty((batch, M, N) if A.dim() == 3 else (M, N), dtype=out_dtype,
                           pin_memory=A.is_pinned())
     out3 = out if out.dim() == 3 else out.unsqueeze(0)
-    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k, multicast=multicast)
+    o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k, multicast=multicast,
+                 tile=tile)
     st = lib.gemm_epilogue_host(batch, M, N, K, la, lb, A3.data_ptr(), lda, sA, B3.data_ptr(), ldb, sB,
                                 bias.data_ptr() if bias is not None else None, sbias, out3.data_ptr(),
                                 max(out3.stride(1), N, 1), out3.stride(0), _op(op, bias), ctypes.byref(o),
@@ -445,12 +481,12 @@ def debug_stats(max_ctas: int = 148):
     """Per-CTA blocked-cycle counters of the last launch (needs GE_DEBUG_STATS=1), as a list of
     dicts, or [] when diagnostics are off.  Synchronizes."""
     import numpy as np
-    buf = np.zeros((max_ctas, 16), dtype=np.uint64)
+    buf = np.zeros((max_ctas, 20), dtype=np.uint64)
     n = load_library().ge_debug_read(buf.ctypes.data, max_ctas)
     keys = ("total", "prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0",
             "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math", "sk_owner_wait", "sk_partial_write",
-            "sk_pieces", "epi_end", "reserved", "first_mma")
-    return [dict(zip(keys, (int(x) for x in buf[i, :16]))) for i in range(n)]
+            "sk_pieces", "epi_end", "reserved", "first_mma", "g_entry", "g_start", "g_epi_end", "g_exit")
+    return [dict(zip(keys, (int(x) for x in buf[i, :20]))) for i in range(n)]
 
 
 def version() -> str:

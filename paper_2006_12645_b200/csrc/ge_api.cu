@@ -116,7 +116,9 @@ ge_status validate_options(const Args& a) {
     if ((a.la != GE_ROW_MAJOR && a.la != GE_COL_MAJOR) || (a.lb != GE_ROW_MAJOR && a.lb != GE_COL_MAJOR))
         return fail(GE_ERR_INVALID_VALUE, "layout must be GE_ROW_MAJOR or GE_COL_MAJOR");
     if (o.bias_mode < GE_BIAS_ROW || o.bias_mode > GE_BIAS_FULL) return fail(GE_ERR_INVALID_VALUE, "bad bias_mode");
-    if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_RELU) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
+    if (o.prologue < GE_PRO_NONE || o.prologue > GE_PRO_HADAMARD) return fail(GE_ERR_INVALID_VALUE, "bad prologue");
+    if (o.ld_prologue_tile < 0 || o.stride_prologue_tile < 0)
+        return fail(GE_ERR_INVALID_VALUE, "negative ld_prologue_tile / stride_prologue_tile");
     if (o.out_dtype != GE_OUT_F16 && o.out_dtype != GE_OUT_F32) return fail(GE_ERR_INVALID_VALUE, "bad out_dtype");
     if (o.tile_n != 0 && o.tile_n != 64 && o.tile_n != 128 && o.tile_n != 192 && o.tile_n != 256 && o.tile_n != 512)
         return fail(GE_ERR_INVALID_VALUE, "tile_n must be 0, 64, 128, 192, 256 or 512");
@@ -176,6 +178,19 @@ ge_status validate(Args& a) {
     if (has_bias(a.op) && !a.bias) return fail(GE_ERR_INVALID_VALUE, "bias is NULL but the op adds a bias");
     if (a.o.prologue == GE_PRO_SCALE_K && a.K > 0 && !a.o.prologue_scale)
         return fail(GE_ERR_INVALID_VALUE, "prologue_scale is NULL for GE_PRO_SCALE_K");
+    if (a.o.prologue == GE_PRO_HADAMARD && a.K > 0) {
+        // S: M x K in A's layout (DESIGN.md R-C18), read with 16-byte vector loads like A
+        if (!a.o.prologue_tile) return fail(GE_ERR_INVALID_VALUE, "prologue_tile is NULL for GE_PRO_HADAMARD");
+        const int64_t minlds = arow ? a.K : a.M;
+        if (a.o.ld_prologue_tile == 0) a.o.ld_prologue_tile = std::max<int64_t>(minlds, 1);
+        if (a.o.ld_prologue_tile < minlds) return fail(GE_ERR_INVALID_VALUE, "ld_prologue_tile too small");
+        if (a.batch > 1 && a.o.stride_prologue_tile != 0 &&
+            a.o.stride_prologue_tile < (arow ? a.M : a.K) * a.o.ld_prologue_tile)
+            return fail(GE_ERR_INVALID_VALUE, "stride_prologue_tile smaller than one item");
+        if ((reinterpret_cast<uintptr_t>(a.o.prologue_tile) & 15) || (a.o.ld_prologue_tile * 2) % 16 ||
+            (a.o.stride_prologue_tile * 2) % 16)
+            return fail(GE_ERR_MISALIGNED, "prologue_tile must be 16-byte aligned with ld/stride multiples of 8 elements");
+    }
     if (a.K2 < 0 || a.K2 > kMaxDim) return fail(GE_ERR_INVALID_VALUE, "K2 out of range");
     if (a.K2 > 0) {
         if (a.o.prologue != GE_PRO_NONE)
@@ -217,8 +232,13 @@ ge_status validate(Args& a) {
         else nBias = extent_bytes(a.batch, a.M, a.N, a.o.ldbias, a.sBias, 2);
     }
     const int64_t nS = (a.o.prologue == GE_PRO_SCALE_K) ? a.K * 4 : 0;
+    const int64_t nT = (a.o.prologue == GE_PRO_HADAMARD && a.K)
+                           ? extent_bytes(a.o.stride_prologue_tile ? a.batch : 1, outerA, arow ? a.K : a.M,
+                                          a.o.ld_prologue_tile, a.o.stride_prologue_tile, 2)
+                           : 0;
     if (overlap(a.C, nC, a.A, a.K ? nA : 0) || overlap(a.C, nC, a.B, a.K ? nB : 0) ||
-        overlap(a.C, nC, a.bias, nBias) || overlap(a.C, nC, a.o.prologue_scale, nS))
+        overlap(a.C, nC, a.bias, nBias) || overlap(a.C, nC, a.o.prologue_scale, nS) ||
+        overlap(a.C, nC, a.o.prologue_tile, nT))
         return fail(GE_ERR_ALIASING, "C overlaps an input buffer");
     return GE_OK;
 }
@@ -454,14 +474,14 @@ unsigned long long* debug_buffer(int sms) {
     cudaGetDevice(&dev);
     dev &= 63;
     if (!g_dbg[dev]) {
-        if (cudaMalloc(&g_dbg[dev], sizeof(unsigned long long) * 16 * sms) != cudaSuccess) {
+        if (cudaMalloc(&g_dbg[dev], sizeof(unsigned long long) * ge::DBG_SLOTS * sms) != cudaSuccess) {
             cudaGetLastError();
             g_dbg[dev] = nullptr;
             return nullptr;
         }
         g_dbg_ctas[dev] = sms;
     }
-    cudaMemset(g_dbg[dev], 0, sizeof(unsigned long long) * 16 * g_dbg_ctas[dev]);
+    cudaMemset(g_dbg[dev], 0, sizeof(unsigned long long) * ge::DBG_SLOTS * g_dbg_ctas[dev]);
     g_dbg_last = dev;
     return g_dbg[dev];
 }
@@ -650,6 +670,13 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.scale = a.o.prologue == GE_PRO_SCALE_K ? a.o.prologue_scale : nullptr;
     p.prologue = a.o.prologue;
     p.scale_vec = p.scale && (reinterpret_cast<uintptr_t>(p.scale) % 16 == 0);
+    // the prologue kernels' transform warps load A (and S) themselves
+    p.a = static_cast<const __half*>(a.A);
+    p.lda = a.lda;
+    p.stride_a = a.sA;
+    p.s_tile = a.o.prologue == GE_PRO_HADAMARD ? static_cast<const __half*>(a.o.prologue_tile) : nullptr;
+    p.lds = a.o.ld_prologue_tile;
+    p.stride_s = a.o.stride_prologue_tile;
     p.C = a.C;
     p.ldc = a.ldc;
     p.stride_c = a.sC;
@@ -709,7 +736,7 @@ Args make_args(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t la, int32
                int64_t ldc, int64_t sC, int32_t op, const ge_options* opt) {
     Args a{batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op, {}};
     if (opt) a.o = *opt;
-    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0};
+    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0, nullptr, 0, 0};
     return a;
 }
 
@@ -838,12 +865,17 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
         else nBias = extent_bytes(a.batch, a.M, a.N, a.o.ldbias, a.sBias, 2);
     }
     const int64_t nS = (a.o.prologue == GE_PRO_SCALE_K && a.K) ? a.K * 4 : 0;
+    // Hadamard prologue tile S (A's layout): copied whole, up front like B
+    const int64_t nT = (a.o.prologue == GE_PRO_HADAMARD && a.K)
+                           ? extent_bytes(a.o.stride_prologue_tile ? a.batch : 1, arow ? a.M : a.K, arow ? a.K : a.M,
+                                          a.o.ld_prologue_tile, a.o.stride_prologue_tile, 2)
+                           : 0;
     const int64_t nC = extent_bytes(a.batch, a.M, a.N, a.ldc, a.sC, es);
     auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
     // stream-K workspace of the launches below (one fp32 128 x 256 slot and one flag per CTA,
     // zero-filled once when allocated; every launch leaves the flags at zero)
     const int64_t nSK = up(static_cast<int64_t>(sms) * (128 * 256 * 4 + 4));
-    const size_t need = nSK + up(nA) + up(nB) + up(nBias) + up(nS) + up(nC);
+    const size_t need = nSK + up(nA) + up(nB) + up(nBias) + up(nS) + up(nT) + up(nC);
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_ws_mu);
@@ -872,7 +904,8 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
     char* dB = dA + up(nA);
     char* dBias = dB + up(nB);
     char* dS = dBias + up(nBias);
-    char* dC = dS + up(nS);
+    char* dT = dS + up(nS);
+    char* dC = dT + up(nT);
     // Pipelined end-to-end path: B, bias and scale go first, then A and C
     // move in blocks (rows of A / C, or whole batch items) so that the GEMM and the C read-back of
     // one block overlap the host->device copy of the next (separate copy engines per direction).
@@ -890,6 +923,8 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
     if (nBias && !chk(cudaMemcpyAsync(dBias, a.bias, nBias, cudaMemcpyHostToDevice, ps.h2d), "H2D bias"))
         return GE_ERR_CUDA;
     if (nS && !chk(cudaMemcpyAsync(dS, a.o.prologue_scale, nS, cudaMemcpyHostToDevice, ps.h2d), "H2D scale"))
+        return GE_ERR_CUDA;
+    if (nT && !chk(cudaMemcpyAsync(dT, a.o.prologue_tile, nT, cudaMemcpyHostToDevice, ps.h2d), "H2D prologue tile"))
         return GE_ERR_CUDA;
     // blocks: batch items when batched, else row blocks (multiples of the 256-row pair tile)
     const bool by_item = a.batch > 1;
@@ -927,8 +962,10 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
         d.o.workspace_bytes = nSK;
         d.B = nB ? dB : nullptr;
         d.o.prologue_scale = nS ? reinterpret_cast<const float*>(dS) : nullptr;
+        d.o.prologue_tile = nT ? dT : nullptr;
         if (by_item) {
             d.batch = u1 - u0;
+            if (nT && a.o.stride_prologue_tile) d.o.prologue_tile = dT + u0 * a.o.stride_prologue_tile * 2;
             d.A = nA ? dA + u0 * a.sA * 2 : nullptr;
             d.B = nB ? dB + u0 * a.sB * 2 : nullptr;
             d.C = dC + u0 * a.sC * es;
@@ -936,6 +973,7 @@ ge_status gemm_epilogue_host(int64_t batch, int64_t M, int64_t N, int64_t K, int
         } else {
             d.M = u1 - u0;
             d.A = nA ? dA + (arow ? u0 * a.lda : u0) * 2 : nullptr;
+            if (nT) d.o.prologue_tile = dT + (arow ? u0 * a.o.ld_prologue_tile : u0) * 2;
             d.C = dC + u0 * a.ldc * es;
             d.bias = nullptr;
             if (nBias) {
@@ -1032,7 +1070,7 @@ void ge_tensor_map_cache_stats(uint64_t* hits, uint64_t* misses) {
 int32_t ge_debug_read(uint64_t* out, int32_t max_ctas) {
     if (g_dbg_last < 0 || !g_dbg[g_dbg_last] || !out) return 0;
     const int n = std::min(max_ctas, g_dbg_ctas[g_dbg_last]);
-    if (cudaMemcpy(out, g_dbg[g_dbg_last], sizeof(uint64_t) * 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    if (cudaMemcpy(out, g_dbg[g_dbg_last], sizeof(uint64_t) * ge::DBG_SLOTS * n, cudaMemcpyDeviceToHost) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }

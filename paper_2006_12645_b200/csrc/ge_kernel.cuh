@@ -72,7 +72,7 @@ constexpr int kXformWarps = 4;
 constexpr int kStagingSetBytes = 16384; // one staging buffer per epilogue warp: 8 x 2 KB (fp16) or 4 x 4 KB (fp32)
 
 enum : int { BIAS_NONE = -1, BIAS_ROW = 0, BIAS_COL = 1, BIAS_FULL = 2 };
-enum : int { PRO_NONE = 0, PRO_SCALE_K = 1, PRO_RELU = 2 };
+enum : int { PRO_NONE = 0, PRO_SCALE_K = 1, PRO_RELU = 2, PRO_HADAMARD = 3 };
 enum : int { ACT_NONE = 0, ACT_RELU = 1, ACT_SIGMOID = 2, ACT_TANH = 3 };
 
 struct Params {
@@ -89,10 +89,17 @@ struct Params {
     int act;                        // ACT_* applied at the root of the epilogue
     float bias_sign;                // +1 add, -1 subtract the bias
     int literal;                    // paper-literal rounding point (DESIGN.md R-C3): fp16(fp16(acc) +- bias)
-    // prologue
-    const float* scale;
+    // prologue (PRO kernels): the transform warps read A from global memory themselves (A is not
+    // TMA-loaded), apply the op in registers and store the swizzled stage: "performed during the
+    // data movement", PAPER.md:1215-1231 (one smem write per element instead of TMA write + read +
+    // write back)
+    const float* scale;             // SCALE_K: s[k], fp32
     int prologue;                   // PRO_*
     int scale_vec;
+    const __half* a;                // A (logical M x K, layout of the kernel's A_MN), leading dim, batch stride
+    long long lda, stride_a;
+    const __half* s_tile;           // HADAMARD: S, same layout as A (M x K fp16), leading dim, batch stride
+    long long lds, stride_s;
     // output
     void* C;
     long long ldc, stride_c;
@@ -122,7 +129,16 @@ struct Params {
 enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
              DBG_EPI_REL0 = 5, DBG_EPI_REL1 = 6, DBG_EPI_TILE = 7, DBG_EPI_TMEMLD = 8,
              DBG_EPI_MATH = 9, DBG_SK_WAIT = 10, DBG_SK_WRITE = 11, DBG_SK_PIECES = 12, DBG_EPI_END = 13,
-             DBG_MMA_END = 14, DBG_FIRST_MMA = 15, DBG_SLOTS = 16 };
+             DBG_MMA_END = 14, DBG_FIRST_MMA = 15,
+             // %globaltimer (ns) of: kernel entry, end of setup (barriers, TMEM, cluster sync), the end
+             // of this CTA's epilogue, and its exit (after teardown)
+             DBG_G_ENTRY = 16, DBG_G_START = 17, DBG_G_EPI_END = 18, DBG_G_EXIT = 19, DBG_SLOTS = 20 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int BN, int CG>
 struct Cfg {
@@ -298,6 +314,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     constexpr int HALF_COLS = BN / NH;
     constexpr uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, C_::kUmmaN, A_MN, B_MN);
 
+    const unsigned long long g_entry = GE_DBG ? globaltimer() : 0ull;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms, by pointer arithmetic on the __shared__ array so
     // the compiler keeps the shared address space (LDS/STS instead of generic LD/ST)
@@ -370,6 +387,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #pragma unroll
     for (int i = 0; i < DBG_SLOTS; ++i) dl[i] = 0;
     const long long t_start = clock64();
+    if (dbg && warp == 1 && lane == 0) {
+        dl[DBG_G_ENTRY] = g_entry;
+        dl[DBG_G_START] = globaltimer();
+    }
     const int cluster_id = blockIdx.x / CL;
     const int num_clusters = gridDim.x / CL;
     const int nkb = p.num_k_blocks;
@@ -403,23 +424,28 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     uint8_t* sb = smem_b + s * C_::kBStage;
                     if (GE_DBG && p.dbg_noload && (wi != 0 || kb >= S)) {
                         // timing experiment (GE_DEBUG_NOLOAD): operands stay resident, results invalid
-                        if (CG == 1 || PRO || leader) ptx::mbar_arrive(&full_bar[s]);
+                        if (CG == 1 || leader) ptx::mbar_arrive(&full_bar[s]);
                         if (++s == S) { s = 0; phase ^= 1; }
                         continue;
                     }
-                    if constexpr (CG == 2 && !PRO) {
+                    // PRO kernels: the transform warps write the A stage; the TMA brings B only
+                    constexpr uint32_t kTx = PRO ? C_::kBStage : C_::kStageBytes;
+                    if constexpr (CG == 2) {
                         // The peer's bytes can only land after the leader's barrier entered this
                         // phase (the peer first waits on its empty[s], released by the MMA that
                         // consumed the previous phase), so a transiently negative tx-count is safe.
-                        if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * C_::kStageBytes);
+                        if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * kTx);
                     } else {
-                        ptx::mbar_arrive_expect_tx(&full_bar[s], C_::kStageBytes);
+                        ptx::mbar_arrive_expect_tx(&full_bar[s], kTx);
                     }
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
-                        if constexpr (CG == 2 && !PRO) ptx::tma_load_3d_pair(dst, map, &full_bar[s], c0, c1, b, pol);
+                        if constexpr (CG == 2) ptx::tma_load_3d_pair(dst, map, &full_bar[s], c0, c1, b, pol);
                         else ptx::tma_load_3d(dst, map, &full_bar[s], c0, c1, b, pol);
                     };
-                    if constexpr (A_MN) {
+                    if constexpr (PRO) {
+                        (void)sa;
+                        (void)pol_a;
+                    } else if constexpr (A_MN) {
 #pragma unroll
                         for (int i = 0; i < kRowsPerCta / 64; ++i) load(sa + i * 8192, map_a, m0 + i * 64, k0, pol_a);
                     } else {
@@ -458,7 +484,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // in uniform registers); one elected lane issues each tcgen05 instruction.  The tensor
             // pipe queues only about one MMA, so the code between consecutive MMAs (barrier wait,
             // fence, commit) is kept minimal: it shows up directly as tensor idle time.
-            uint64_t* const ready = PRO ? xform_bar : full_bar;
+            // stage s is ready when its TMA bytes landed (full) and, with a prologue, when the
+            // transform warps of both CTAs stored its A (xform)
+            auto wait_ready = [&](int st, uint32_t ph, unsigned long long& acc) {
+                ptx::mbar_wait_timed(&full_bar[st], ph, dbg && lane == 0, acc);
+                if constexpr (PRO) ptx::mbar_wait_timed(&xform_bar[st], ph, dbg && lane == 0, acc);
+            };
             const uint32_t a_base = ptx::smem_u32(smem_a);
             const uint32_t b_base = ptx::smem_u32(smem_b);
             int s = 0, it = 0;
@@ -514,7 +545,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             }
                             npend = 0;
                         }
-                        ptx::mbar_wait_timed(&ready[s], phase, dbg && lane == 0, dl[DBG_MMA_FULL]);
+                        wait_ready(s, phase, dl[DBG_MMA_FULL]);
                         ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             ptx::mbar_wait_timed(&tempty_bar[0], acc_phase ^ 1,
@@ -548,8 +579,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
                 } else {
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
-                        if (!(GE_EARLY_TEST && next_ready))
-                            ptx::mbar_wait_timed(&ready[s], phase, dbg && lane == 0, dl[DBG_MMA_FULL]);
+                        if (!(GE_EARLY_TEST && next_ready)) wait_ready(s, phase, dl[DBG_MMA_FULL]);
                         ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             // first k-block of a tile: the epilogue must have drained this buffer
@@ -561,7 +591,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             // readiness of the next stage, tested before this stage's MMAs are issued
                             // so the barrier round trip overlaps the issue
                             const int sn = s + 1 == S ? 0 : s + 1;
-                            next_ready = ptx::mbar_test(&ready[sn], s + 1 == S ? phase ^ 1 : phase);
+                            next_ready = ptx::mbar_test(&full_bar[sn], s + 1 == S ? phase ^ 1 : phase) &&
+                                         (!PRO || ptx::mbar_test(&xform_bar[sn], s + 1 == S ? phase ^ 1 : phase));
                         }
                         mma_half(s, kb, 0);
                         release_stage(s);                         // smem slot free once these MMAs finish
@@ -1066,64 +1097,108 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             if (GE_END_WAIT_READ) ptx::bulk_wait_read<0>();
             else ptx::bulk_wait<0>();
         }
-        if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
+        if (dbg && e_idx == 0 && lane == 0) {
+            dl[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
+            dl[DBG_G_EPI_END] = globaltimer();
+        }
     } else if (PRO && warp >= 4 + EPI_WARPS) {
-        // ===================== prologue transform of the A stage (in place, in smem) ==========
+        // ===================== prologue: A global -> registers -> op -> swizzled smem stage ===========
+        // Sec. VII-C: the pointwise op is applied while A moves from global to
+        // shared memory, on register-staged data (the paper's Volta copy path), so the
+        // stage costs ONE smem write per element (a TMA load + in-place rewrite costs three).  The
+        // warps run ahead of the MMA by the ring depth; loads for the next k-block are issued as soon
+        // as the current one is stored, so their latency overlaps the wait for the next free slot.
+        //  K-major stage (A row-major; 128 rows x 128 B, 128-B swizzle): thread xt owns the logical
+        //   k-chunk c = xt % 8 of rows r_i = xt / 8 + 16 i (i < 8), stored at r_i * 128 +
+        //   ((c ^ (r_i % 8)) * 16): its 8 chunks share one 8-wide k range (one set of scale values);
+        //   a warp stores 4 whole 128-B rows (conflict-free) and loads 4 whole 128-B row segments.
+        //  MN-major stage (A col-major; two 64-m atoms of 64 k-rows x 128 B): thread xt owns the
+        //   m-chunk c = xt % 16 (atom c / 8) of k-rows k_i = xt / 16 + 8 i, stored at
+        //   (c / 8) * 8192 + k_i * 128 + (((c % 8) ^ (k_i % 8)) * 16).
+        // Out-of-range rows / k (tile tails) are zero-filled like the TMA path (the K tail adds 0).
         const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
-        // Thread xt rewrites the 16-B chunks o = (i*128 + xt)*16, i = 0..7, of each 16 KB A stage.
-        //  K-major stage (row = m, 128-B rows of 64 k, 128-B swizzle): the logical k-chunk of all
-        //   eight chunks is kc = (xt % 8) ^ ((xt / 8) % 8), so the thread needs scale[k0+8kc .. +8];
-        //  MN-major stage (row = k, 64-m atoms of 8 KB): chunk i lies on k = k0 + (16i + xt/8) % 64.
-        // The 8 scale values of the NEXT k-block are prefetched while the current one is
-        // transformed (the scale vector would otherwise cost an L2 round trip per chunk).
-        const bool scale_k = p.prologue == PRO_SCALE_K;
-        const int kc = (xt & 7) ^ ((xt >> 3) & 7);
-        auto fetch = [&](int kb, float* dst) {
-            const int k0 = kb * kBK;
-            if constexpr (A_MN) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = k0 + ((i * 16 + (xt >> 3)) & 63);
-                    dst[i] = k < p.K ? __ldg(p.scale + k) : 0.0f;
-                }
-            } else {
-                const int k = k0 + kc * 8;
-                if (p.scale_vec && k + 8 <= p.K) {
-                    const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + k));
-                    const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + k + 4));
-                    dst[0] = s0.x; dst[1] = s0.y; dst[2] = s0.z; dst[3] = s0.w;
-                    dst[4] = s1.x; dst[5] = s1.y; dst[6] = s1.z; dst[7] = s1.w;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) dst[e] = (k + e < p.K) ? __ldg(p.scale + k + e) : 0.0f;
-                }
-            }
+        constexpr int NCH = C_::kAStage / 16 / 128;          // 8 chunks of 16 B per thread
+        const int op = p.prologue;
+        const bool had = op == PRO_HADAMARD;
+        uint4 xa[NCH], xs[NCH];                               // A (and S) chunks of the next k-block
+        float sc[NCH];                                        // SCALE_K factors of those chunks
+        // 8 consecutive fp16 of row-major / col-major storage at element offset `off` of base, the
+        // first `valid` of them in range (0..8); 16-B aligned when valid == 8
+        auto ld8 = [&](const __half* base, long long off, int valid) -> uint4 {
+            if (valid >= 8) return __ldg(reinterpret_cast<const uint4*>(base + off));
+            uint4 r = make_uint4(0u, 0u, 0u, 0u);
+            __half* h = reinterpret_cast<__half*>(&r);
+            for (int e = 0; e < valid; ++e) h[e] = base[off + e];
+            return r;
         };
-        float sc_cur[8], sc_nxt[8];
-        if (scale_k && nkb > 0 && work.count() > 0) fetch(work.get(0).kb0, sc_nxt);
-        int s = 0;
-        uint32_t phase = 0;
-        for (int wi = 0; wi < work.count(); ++wi) {
+        int wi_l = 0, kb_l = 0;                               // the k-block the registers hold
+        auto load = [&](int wi, int kb) {
             const Piece pc = work.get(wi);
-            for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
-                if (scale_k) {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) sc_cur[e] = sc_nxt[e];
-                    int kn = kb + 1;                                  // next k-block this thread transforms
-                    if (kn == pc.kb1) kn = (wi + 1 < work.count()) ? work.get(wi + 1).kb0 : 0;
-                    fetch(kn, sc_nxt);                                // in flight during this stage
-                }
-                ptx::mbar_wait(&full_bar[s], phase);
-                uint8_t* sa = smem_a + s * C_::kAStage;
-                constexpr int NCH = C_::kAStage / 16 / 128;          // 8 chunks per thread
-                uint4 x[NCH];
-#pragma unroll
-                for (int i = 0; i < NCH; ++i) x[i] = *reinterpret_cast<const uint4*>(sa + (i * 128 + xt) * 16);
+            int b, mt, nt;
+            decode_tile(p, pc.tile, TILE_M, b, mt, nt);
+            const int m0 = mt * TILE_M + rank * kRowsPerCta;
+            const int k0 = kb * kBK;
+            const __half* A = p.a + static_cast<long long>(b) * p.stride_a;
+            const __half* Sm = had ? p.s_tile + static_cast<long long>(b) * p.stride_s : nullptr;
+            if constexpr (!A_MN) {
+                const int k = k0 + (xt & 7) * 8;
+                const int kv = max(0, min(8, p.K - k));
 #pragma unroll
                 for (int i = 0; i < NCH; ++i) {
-                    if (!scale_k) {
-                        // RELU: a' = max(a, +0): clear every lane with the sign bit set (exact, -0 -> +0)
-                        uint32_t* w = reinterpret_cast<uint32_t*>(&x[i]);
+                    const int m = m0 + (xt >> 3) + 16 * i;
+                    const int v = m < p.M ? kv : 0;
+                    xa[i] = ld8(A, static_cast<long long>(m) * p.lda + k, v);
+                    if (had) xs[i] = ld8(Sm, static_cast<long long>(m) * p.lds + k, v);
+                }
+                if (op == PRO_SCALE_K) {
+                    if (p.scale_vec && kv == 8) {
+                        const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + k));
+                        const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + k + 4));
+                        sc[0] = s0.x; sc[1] = s0.y; sc[2] = s0.z; sc[3] = s0.w;
+                        sc[4] = s1.x; sc[5] = s1.y; sc[6] = s1.z; sc[7] = s1.w;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) sc[e] = e < kv ? __ldg(p.scale + k + e) : 0.0f;
+                    }
+                }
+            } else {
+                const int m = m0 + (xt & 15) * 8;
+                const int mv = max(0, min(8, p.M - m));
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) {
+                    const int k = k0 + (xt >> 4) + 8 * i;
+                    const int v = k < p.K ? mv : 0;
+                    xa[i] = ld8(A, static_cast<long long>(k) * p.lda + m, v);
+                    if (had) xs[i] = ld8(Sm, static_cast<long long>(k) * p.lds + m, v);
+                    if (op == PRO_SCALE_K) sc[i] = k < p.K ? __ldg(p.scale + k) : 0.0f;
+                }
+            }
+            wi_l = wi;
+            kb_l = kb;
+        };
+        auto advance = [&](int& wi, int& kb) {           // next k-block in the work sequence
+            if (++kb == work.get(wi).kb1) {
+                ++wi;
+                kb = (wi < work.count()) ? work.get(wi).kb0 : 0;
+            }
+        };
+        int s = 0;
+        uint32_t phase = 0;
+        if (nkb > 0 && work.count() > 0) {
+            int wi = 0, kb = work.get(0).kb0;
+            load(wi, kb);
+            while (wi < work.count()) {
+                // the slot is free once the MMAs that read its previous contents completed (paired
+                // release: the odd stage's commit covers the even one, as for the TMA producer)
+                if (!GE_PAIR_RELEASE) ptx::mbar_wait(&empty_bar[s], phase ^ 1);
+                else if ((s & 1) == 0) ptx::mbar_wait(&empty_bar[s + 1], phase ^ 1);
+                uint4 y[NCH];
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) {
+                    y[i] = xa[i];
+                    uint32_t* w = reinterpret_cast<uint32_t*>(&y[i]);
+                    if (op == PRO_RELU) {
+                        // a' = max(a, +0): clear every lane with the sign bit set (exact, -0 -> +0)
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             uint32_t u = w[e];
@@ -1131,29 +1206,55 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             if (u & 0x80000000u) u &= 0x0000FFFFu;
                             w[e] = u;
                         }
-                    } else {
-                        // SCALE_K: a' = RNE_fp16(s_k * a) (DESIGN.md R-C12)
-                        __half2* h2 = reinterpret_cast<__half2*>(&x[i]);
+                    } else if (op == PRO_SCALE_K) {
+                        // a' = RNE_fp16(s_k * a) (DESIGN.md R-C12)
+                        __half2* h2 = reinterpret_cast<__half2*>(&y[i]);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float2 a = __half22float2(h2[e]);
-                            const float s0 = A_MN ? sc_cur[i] : sc_cur[2 * e];
-                            const float s1 = A_MN ? sc_cur[i] : sc_cur[2 * e + 1];
+                            const float s0 = A_MN ? sc[i] : sc[2 * e];
+                            const float s1 = A_MN ? sc[i] : sc[2 * e + 1];
                             h2[e] = __floats2half2_rn(s0 * a.x, s1 * a.y);
                         }
+                    } else if (had) {
+                        // a' = RNE_fp16(s(i,k) * a(i,k)): the fp16 x fp16 product is exact before its
+                        // one rounding (mul.rn.f16x2; DESIGN.md R-C18)
+                        __half2* h2 = reinterpret_cast<__half2*>(&y[i]);
+                        const __half2* s2 = reinterpret_cast<const __half2*>(&xs[i]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) h2[e] = __hmul2(h2[e], s2[e]);
                     }
                 }
+                // registers are free again: issue the next k-block's loads before storing this one
+                int wn = wi, kn = kb;
+                advance(wn, kn);
+                if (wn < work.count()) load(wn, kn);
+                uint8_t* sa = smem_a + s * C_::kAStage;
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) *reinterpret_cast<uint4*>(sa + (i * 128 + xt) * 16) = x[i];
-                ptx::fence_proxy_async_smem();
+                for (int i = 0; i < NCH; ++i) {
+                    int off;
+                    if constexpr (!A_MN) {
+                        const int r = (xt >> 3) + 16 * i;
+                        off = r * 128 + (((xt & 7) ^ (r & 7)) * 16);
+                    } else {
+                        const int c = xt & 15, kk = (xt >> 4) + 8 * i;
+                        off = (c >> 3) * 8192 + kk * 128 + ((((c & 7) ^ (kk & 7))) * 16);
+                    }
+                    *reinterpret_cast<uint4*>(sa + off) = y[i];
+                }
+                ptx::fence_proxy_async_smem();               // generic-proxy stores -> the MMA (async proxy)
                 __syncwarp();
                 if (lane == 0) {
                     if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&xform_bar[s], 0);
                     else ptx::mbar_arrive(&xform_bar[s]);
                 }
                 if (++s == S) { s = 0; phase ^= 1; }
+                wi = wn;
+                kb = kn;
             }
         }
+        (void)wi_l;
+        (void)kb_l;
     }
 
     // ---- teardown: every role done; the allocating warp frees TMEM
@@ -1170,6 +1271,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<CG>(tmem_base, C_::kTmemCols);
+        if (GE_DBG && p.dbg != nullptr && lane == 0) atomicAdd(p.dbg + blockIdx.x * DBG_SLOTS + DBG_G_EXIT, globaltimer());
     }
 #endif
 }

@@ -7,10 +7,14 @@ import paper_2006_12645_b200 as ge
 M, N, K = (int(x) for x in sys.argv[1:4]); lay = sys.argv[4]; bn, cg = int(sys.argv[5]), int(sys.argv[6])
 sk = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 mc = int(sys.argv[8]) if len(sys.argv) > 8 else 0
-A = torch.randn(M, K, device="cuda", dtype=torch.float16); B = torch.randn(K, N, device="cuda", dtype=torch.float16)
-if lay[0] == "c": A = A.t().contiguous().t()
-if lay[1] == "c": B = B.t().contiguous().t()
-bias = torch.randn(N, device="cuda", dtype=torch.float16); C = torch.empty(M, N, device="cuda", dtype=torch.float16)
+ld8 = lambda n: (n + 7) // 8 * 8          # padded leading dimensions (16-byte TMA pitch), like bench.py
+def operand(rows, cols, l):
+    if l == "r":
+        return torch.randn(rows, ld8(cols), device="cuda", dtype=torch.float16)[:, :cols]
+    return torch.randn(cols, ld8(rows), device="cuda", dtype=torch.float16)[:, :rows].t()
+A = operand(M, K, lay[0]); B = operand(K, N, lay[1])
+bias = torch.randn(N, device="cuda", dtype=torch.float16)
+C = torch.empty(M, ld8(N), device="cuda", dtype=torch.float16)[:, :N]
 for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk, multicast=mc)
 torch.cuda.synchronize()
 st = ge.debug_stats()
@@ -31,3 +35,13 @@ for i, r in sorted(enumerate(st), key=lambda x: -x[1]["epi_end"])[:6]:
     print(f"    {i:3d}: {r['epi_end']:7d} {r['total']:7d} {r['sk_owner_wait']:7d} {r['sk_partial_write']:6d} {r['sk_pieces']} {r['epi_tile']:7d}")
 fm = sorted(r["first_mma"] for r in lead)
 print("  first MMA (cycles after kernel start) per leader: min", fm[0], "median", fm[len(fm)//2], "max", fm[-1])
+
+# absolute timeline (%globaltimer, ns) across CTAs: launch stagger, setup, epilogue end, exit
+ent = [r["g_entry"] for r in st if r["g_entry"]]
+if ent:
+    t0 = min(ent)
+    rel = lambda k: sorted(r[k] - t0 for r in st if r[k])
+    for k in ("g_entry", "g_start", "g_epi_end", "g_exit"):
+        v = rel(k)
+        if v:
+            print(f"  {k:10s} ns after first entry: min {v[0]:7d} median {v[len(v)//2]:7d} max {v[-1]:7d} (n={len(v)})")

@@ -21,11 +21,15 @@ def oracle_run(prob: workloads.Problem, layouts: str = "rr", *, relu=True, bias_
     bias_mode = prob.meta.get("bias_mode") if bias_mode is None else bias_mode
     As, lda, Bs, ldb = stored(prob, layouts, lda, ldb)
     ldbias = prob.bias.shape[1] if (prob.bias is not None and prob.bias.dim() == 2) else 0
+    pro = prob.meta.get("prologue")
+    scale, lds = prob.scale, None
+    if pro == "hadamard":          # the tile S is stored in A's layout
+        scale, lds = workloads.store(prob.scale, layouts[0])
     return oracle.gemm_epilogue(
         As, Bs, prob.M, prob.N, prob.K,
         layoutA="row" if layouts[0] == "r" else "col", layoutB="row" if layouts[1] == "r" else "col",
         lda=lda, ldb=ldb, bias=prob.bias, bias_mode=bias_mode if prob.bias is not None else None,
-        ldbias=ldbias, relu=relu, act=act, bias_sub=bias_sub, prologue=prob.meta.get("prologue"), scale=prob.scale,
+        ldbias=ldbias, relu=relu, act=act, bias_sub=bias_sub, prologue=pro, scale=scale, lds=lds,
         literal_round=literal_round, rows=rows, cols=cols, nthreads=nthreads)
 
 

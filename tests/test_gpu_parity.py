@@ -6,14 +6,15 @@ the GPU must equal RNE_fp16(oracle) (fp16 out) or the oracle itself (fp32 out) b
 (DESIGN.md "Parity").  All inputs are seeded (workloads.py)."""
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import workloads
-import json
-import os
 
 from tests.helpers import check_bound, check_relu_invariant, oracle_run
 
@@ -34,10 +35,22 @@ def dev_operands(prob: workloads.Problem, layouts: str, lda=None, ldb=None):
     return put(prob.A, layouts[0], lda), put(prob.B, layouts[1], ldb)
 
 
+def dev_tile(logical, lay, ld=None):
+    """A logical M x K tile on the GPU in layout `lay` (the Hadamard operand S follows A's layout)."""
+    if ld is None:
+        ld = (logical.shape[1 if lay == "r" else 0] + 7) // 8 * 8
+    st, ld = workloads.store(logical, lay, ld)
+    d = st.cuda()
+    R, C = logical.shape
+    return d[:, :C] if lay == "r" else d[:, :R].t()
+
+
 def run_gpu(prob, layouts="rr", *, op=None, out_dtype=torch.float16, lda=None, ldb=None, **kw):
     A, B = dev_operands(prob, layouts, lda, ldb)
     bias = prob.bias.cuda() if prob.bias is not None else None
     scale = prob.scale.cuda() if prob.scale is not None else None
+    if prob.meta.get("prologue") == "hadamard":
+        scale = dev_tile(prob.scale, layouts[0])
     C = ge.gemm_epilogue(A, B, bias, op=op, bias_mode=prob.meta.get("bias_mode") or "row",
                          prologue=prob.meta.get("prologue"), scale=scale, out_dtype=out_dtype, **kw)
     torch.cuda.synchronize()
@@ -146,12 +159,15 @@ def test_epilogue_variants(bias_mode, out_dtype, op):
     assert np.array_equal(got, exact_expect(out, out_dtype))
 
 
-@pytest.mark.parametrize("prologue", ["scale_k", "relu"])
+@pytest.mark.parametrize("prologue", ["scale_k", "relu", "hadamard"])
 @pytest.mark.parametrize("layouts", workloads.LAYOUTS)
-@pytest.mark.parametrize("tile_n,cg", [(256, 1), (256, 2), (64, 1), (512, 2)])
+@pytest.mark.parametrize("tile_n,cg", [(256, 1), (256, 2), (64, 1), (512, 2), (128, 2), (192, 1)])
 def test_prologue(prologue, layouts, tile_n, cg):
-    """Prologue fusion (Sec. VII-C; SCALE_K = DESIGN.md R-C12): exact on small
-    integers with s in {0.5, 1, 2}, within the bound on uniform data."""
+    """Prologue fusion (Sec. VII-C; SCALE_K = DESIGN.md R-C12, HADAMARD = R-C18,
+    the full-tile op with a second input dataspace): the transform warps load A
+    (and S) from global memory, apply the op in registers and store the swizzled stage; exact on
+    small integers (s in {0.5, 1, 2}; S in {-1, 0.5, 1, 2}), within the bound on uniform data, with
+    M/N/K tails (257 x 300 x 200: a partial last row tile and a K tail inside one 16-B chunk)."""
     for kind in ("smallint", "uniform"):
         prob = workloads.make_problem(257, 300, 200, seed=34, kind=kind, bias_mode="row", prologue=prologue)
         got = run_gpu(prob, layouts, tile_n=tile_n, cta_group=cg)
@@ -655,3 +671,51 @@ def test_sharded_world1_is_the_batched_call(bias_mode):
     want = ge.gemm_epilogue(A[0], B[0], b2, bias_mode=bias_mode)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_hadamard_reductions_on_gpu(layouts):
+    """S = 1 gives the plain GEMM bitwise; a column-constant S(i,k) = s_k (fp16 values) gives the
+    SCALE_K prologue with the same s bitwise (both round fp16(s * a) once: the fp16 x fp16 product is
+    exact in fp32); odd K (K tail inside a 16-B chunk) and ld padding of S."""
+    prob = workloads.make_problem(300, 264, 203, seed=96, kind="uniform", bias_mode="row")
+    A, B = dev_operands(prob, layouts)
+    bias = prob.bias.cuda()
+    plain = ge.gemm_epilogue(A, B, bias)
+    ones = dev_tile(torch.ones(300, 203, dtype=torch.float16), layouts[0], ld=216 if layouts[0] == "r" else 304)
+    had1 = ge.gemm_epilogue(A, B, bias, prologue="hadamard", scale=ones)
+    s = workloads.uniform_f16((203,), 97, 0.5, 1.5)
+    colS = dev_tile(s[None, :].expand(300, 203).contiguous(), layouts[0])
+    hadc = ge.gemm_epilogue(A, B, bias, prologue="hadamard", scale=colS)
+    sk = ge.gemm_epilogue(A, B, bias, prologue="scale_k", scale=s.float().cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(had1, plain)
+    assert torch.equal(hadc, sk)
+
+
+def test_hadamard_batched_and_host():
+    """Per-item and shared S in the batched call (item b == the single call on item b, bitwise) and
+    the host-buffer entry (== the device path, bitwise)."""
+    batch, M, N, K = 3, 200, 136, 96
+    probs = [workloads.make_problem(M, N, K, seed=800 + b, kind="uniform", bias_mode="row", prologue="hadamard")
+             for b in range(batch)]
+    A = torch.stack([p.A for p in probs]).cuda()
+    B = torch.stack([p.B for p in probs]).cuda()
+    S = torch.stack([p.scale for p in probs]).cuda()
+    bias = probs[0].bias.cuda()
+    for tile in (S, S[1]):
+        C = ge.gemm_epilogue_batched(A, B, bias, prologue="hadamard", scale=tile)
+        for b in range(batch):
+            Cb = ge.gemm_epilogue(A[b], B[b], bias, prologue="hadamard", scale=tile[b] if tile.dim() == 3 else tile)
+            torch.cuda.synchronize()
+            assert torch.equal(C[b], Cb)
+    p0 = probs[0]
+    out, mag = oracle_run(p0, "rr")
+    got = ge.gemm_epilogue(A[0], B[0], bias, prologue="hadamard", scale=S[0])
+    torch.cuda.synchronize()
+    check_bound(got.float().cpu().numpy(), out, mag, "hadamard item 0")
+    Ch = ge.gemm_epilogue_host(p0.A.pin_memory(), p0.B.pin_memory(), p0.bias.pin_memory(), prologue="hadamard",
+                               scale=p0.scale.pin_memory())
+    Cd = ge.gemm_epilogue(A[0], B[0], bias, prologue="hadamard", scale=S[0])
+    torch.cuda.synchronize()
+    assert torch.equal(Ch, Cd.cpu())

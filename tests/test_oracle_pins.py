@@ -74,6 +74,8 @@ def test_hand_computed_cases(case, layouts):
     B = torch.tensor(case["B"], dtype=torch.float16).reshape(K, N)
     bias = None if case["bias"] is None else torch.tensor(case["bias"], dtype=torch.float16)
     scale = None if case.get("scale") is None else torch.tensor(case["scale"], dtype=torch.float32)
+    if case["prologue"] == "hadamard":
+        scale = torch.tensor(case["S"], dtype=torch.float16).reshape(M, K)
     prob = workloads.Problem(M, N, K, A, B, bias, scale,
                              {"bias_mode": case["bias_mode"], "prologue": case["prologue"]})
     out, mag = oracle_run(prob, layouts, relu=case["relu"], literal_round=case.get("literal_round", False))
@@ -114,6 +116,9 @@ def _exact(prob, relu, bias_mode):
     if prob.meta.get("prologue") == "scale_k":
         s = [Fraction(float(v)) for v in prob.scale.tolist()]
         A = [[s[k] * A[i][k] for k in range(prob.K)] for i in range(prob.M)]
+    elif prob.meta.get("prologue") == "hadamard":
+        S = [[Fraction(float(v)) for v in row] for row in prob.scale.float().tolist()]
+        A = [[S[i][k] * A[i][k] for k in range(prob.K)] for i in range(prob.M)]
     elif prob.meta.get("prologue") == "relu":
         A = [[max(v, Fraction(0)) for v in row] for row in A]
     outs, mags = [], []
@@ -142,9 +147,9 @@ def test_brute_force_exact_rationals():
     (PAPER.md:355-364, 1201-1206): |oracle - exact| <= 1e-12 * mag (fp64 summation)."""
     dims = (1, 2, 3, 5, 8)
     modes = ("row", "col", "full", None)
-    pros = (None, "relu", "scale_k")
+    pros = (None, "relu", "scale_k", "hadamard")
     for n, (M, N, K) in enumerate(itertools.product(dims, dims, dims)):
-        bm, pro, lay = modes[n % 4], pros[n % 3], workloads.LAYOUTS[n % 4]
+        bm, pro, lay = modes[n % 4], pros[(n // 4) % 4], workloads.LAYOUTS[n % 4]
         relu = n % 2 == 0
         prob = workloads.make_problem(M, N, K, seed=1000 + n, bias_mode=bm, prologue=pro)
         out, mag = oracle_run(prob, lay, relu=relu)
@@ -440,3 +445,48 @@ def test_gemm2_reductions():
     a, _ = oracle.gemm2_epilogue(p1.A, p1.B, pb.A, pb.B, M, N, K1, K1, bias=p1.bias, act=None)
     b, _ = oracle.gemm2_epilogue(pb.A, pb.B, p1.A, p1.B, M, N, K1, K1, bias=p1.bias, act=None)
     assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- Hadamard prologue (R-C18)
+def _had(prob, S):
+    return workloads.Problem(prob.M, prob.N, prob.K, prob.A, prob.B, prob.bias, S,
+                             {"bias_mode": prob.meta["bias_mode"], "prologue": "hadamard"})
+
+
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_hadamard_special_cases(layouts):
+    """Full-tile Hadamard prologue a'(i,k) = s(i,k) a(i,k) (DESIGN.md R-C18), pinned
+    by reductions the mathematics fixes: S = 1 is the plain GEMM bitwise; S = 2^p scales the bias-free
+    pre-activation by exactly 2^p; a per-row S(i,k) = 2^p_i scales row i by 2^p_i (a transposed S
+    fails this); a per-column S(i,k) = s_k is the (already pinned) SCALE_K prologue bitwise."""
+    M, N, K = 37, 45, 53
+    prob = workloads.make_problem(M, N, K, seed=95, bias_mode=None)
+    none = oracle_run(prob, layouts, relu=False)[0]
+    assert np.array_equal(oracle_run(_had(prob, torch.ones(M, K, dtype=torch.float16)), layouts, relu=False)[0], none)
+    assert np.array_equal(oracle_run(_had(prob, torch.full((M, K), 0.25, dtype=torch.float16)), layouts,
+                                     relu=False)[0], 0.25 * none)
+    p = torch.randint(-3, 4, (M,), generator=workloads.gen(96))
+    rowS = torch.pow(2.0, p.double())[:, None].expand(M, K).to(torch.float16)
+    got = oracle_run(_had(prob, rowS), layouts, relu=False)[0]
+    assert np.array_equal(got, np.exp2(p.double().numpy())[:, None] * none)
+    # control: the same exponents applied along k instead of i do not give the row-scaled result
+    q = torch.randint(-3, 4, (K,), generator=workloads.gen(99))
+    kS = torch.pow(2.0, q.double())[None, :].expand(M, K).to(torch.float16)
+    assert not np.array_equal(oracle_run(_had(prob, kS), layouts, relu=False)[0], got)
+    s = workloads.uniform_f16((K,), 97, 0.5, 1.5)
+    colS = s[None, :].expand(M, K).contiguous()
+    sk = workloads.Problem(M, N, K, prob.A, prob.B, None, s.float(), {"bias_mode": None, "prologue": "scale_k"})
+    assert np.array_equal(oracle_run(_had(prob, colS), layouts, relu=False)[0], oracle_run(sk, layouts, relu=False)[0])
+
+
+def test_hadamard_numpy_crosscheck():
+    """(A * S) @ B + bias, relu, in numpy fp64 on a ragged shape, every layout of A (S follows A)."""
+    prob = workloads.make_problem(70, 90, 110, seed=98, bias_mode="row", prologue="hadamard")
+    A = prob.A.numpy().astype(np.float64) * prob.scale.numpy().astype(np.float64)
+    B = prob.B.numpy().astype(np.float64)
+    pre = A @ B + prob.bias.numpy().astype(np.float64)[None, :]
+    ref, rmag = np.where(pre > 0, pre, 0.0), np.abs(A) @ np.abs(B)
+    for lay in workloads.LAYOUTS:
+        out, mag = oracle_run(prob, lay)
+        assert np.all(np.abs(out - ref) <= 1e-12 * rmag + 1e-300), lay
+        assert np.allclose(mag, rmag, rtol=1e-12, atol=0)

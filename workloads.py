@@ -11,6 +11,8 @@ Input recipe: the paper gives sizes only (PAPER.md:1249-125
     then rounded to fp16 (RNE) -> identical bits on every machine.
   * "smallint": a, b ~ U{-3..3}, bias ~ U{-8..8} (exact-arithmetic pin).
   * prologue scale s ~ U(0.5, 1.5) fp32 (uniform) or s in {0.5, 1, 2} (smallint).
+  * Hadamard prologue tile S (M x K fp16): U(0.5, 1.5) rounded to fp16 (uniform) or
+    S in {-1, 0.5, 1, 2} (smallint: every a*s is exact in fp16 and the sums stay exact in fp32).
 """
 from __future__ import annotations
 
@@ -44,6 +46,15 @@ def scale_vector(K: int, seed: int, kind: str = "uniform") -> torch.Tensor:
         choices = torch.tensor([0.5, 1.0, 2.0], dtype=torch.float32)
         return choices[torch.randint(0, 3, (K,), generator=g)]
     return torch.rand((K,), generator=g, dtype=torch.float32) + 0.5
+
+
+def hadamard_tile(M: int, K: int, seed: int, kind: str = "uniform") -> torch.Tensor:
+    """Logical M x K fp16 tile S of the Hadamard prologue (a'(i,k) = S[i,k] * A[i,k])."""
+    g = gen(seed)
+    if kind == "smallint":
+        choices = torch.tensor([-1.0, 0.5, 1.0, 2.0], dtype=torch.float32)
+        return choices[torch.randint(0, 4, (M, K), generator=g)].to(torch.float16)
+    return (torch.rand((M, K), generator=g, dtype=torch.float32) + 0.5).to(torch.float16)
 
 
 def store(logical: torch.Tensor, layout: str, ld: Optional[int] = None) -> tuple[torch.Tensor, int]:
@@ -97,8 +108,11 @@ def make_problem(M: int, N: int, K: int, seed: int, kind: str = "uniform", bias_
         bias[:, :N] = mk_bias((M, N))
     else:
         raise ValueError(bias_mode)
-    scale = scale_vector(K, seed * 7 + 4, "smallint" if kind == "smallint" else "uniform") \
-        if prologue == "scale_k" else None
+    scale = None
+    if prologue == "scale_k":
+        scale = scale_vector(K, seed * 7 + 4, "smallint" if kind == "smallint" else "uniform")
+    elif prologue == "hadamard":
+        scale = hadamard_tile(M, K, seed * 7 + 5, kind)
     return Problem(M, N, K, A, B, bias, scale, {"seed": seed, "kind": kind, "bias_mode": bias_mode,
                                                 "prologue": prologue})
 
