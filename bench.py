@@ -47,6 +47,7 @@ WORKLOADS = {
     "deepbench_a": (1, 5124, 700, 2048, ("rr", "rc"), None),
     "deepbench_b": (1, 35, 8457, 2560, ("rr", "rc"), None),
     "prologue4096": (1, 4096, 4096, 4096, ("rr",), "scale_k"),
+    "hadamard4096": (1, 4096, 4096, 4096, ("rr",), "hadamard"),
     "batched64x2048": (64, 2048, 2048, 2048, ("rr",), None),
 }
 
@@ -242,7 +243,7 @@ def algorithmic_bytes(batch, M, N, K, pro):
     (bench uses one per item for batches, one shared otherwise) and the SCALE_K vector."""
     per_item = 2 * M * K + 2 * K * N + 2 * M * N
     bias = 2 * N * (batch if batch > 1 else 1)
-    return batch * per_item + bias + (4 * K if pro == "scale_k" else 0)
+    return batch * per_item + bias + (4 * K if pro == "scale_k" else 0) + (2 * M * K if pro == "hadamard" else 0)
 
 
 class Workload:
@@ -293,6 +294,10 @@ class Workload:
         else:
             self.bias = U(N, seed=1000 + rank + 31)
         self.scale = (torch.rand(K, generator=g, device=dev) + 0.5) if pro == "scale_k" else None
+        if pro == "hadamard":          # the M x K tile S, stored in A's layout, U(0.5, 1.5)
+            lay = layouts[0][0]
+            S = (torch.rand((M, ld8(K)) if lay == "r" else (K, ld8(M)), generator=g, device=dev) + 0.5).half()
+            self.scale = S[:, :K] if lay == "r" else S[:, :M].t()
         self.C = torch.empty(max(batch, 1), M, ld8(N), dtype=torch.float16, device=dev)[:batch, :, :N]
         self.step_no = 0
         self.graphs = None

@@ -124,7 +124,13 @@ typedef struct {
                                        stride_prologue_tile * 2 multiples of 16 (else GE_ERR_MISALIGNED) */
     int64_t ld_prologue_tile;       /* leading dimension of S in elements (0 = packed: K row-major, M col-major) */
     int64_t stride_prologue_tile;   /* batched: element stride between items' S (0 = one S shared by all) */
-} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0, NULL, 0, 0} */
+    int32_t swap_ab;                /* 0 = heuristic; 1 = never; 2 = always where legal.  Swap-AB computes
+                                       C^T = B^T A^T (the long N side becomes the 128-row MMA side, the
+                                       skinny M side the MMA N) and stores C transposed; used for skinny
+                                       M (<= 64) with ROW/COL/no bias, no prologue, no sum of matmuls
+                                       (DESIGN.md "Skinny shapes").  Results stay within the bound; the
+                                       summation order may differ from the unswapped launch. */
+} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0, NULL, 0, 0, 0} */
 
 typedef enum {
     GE_OK = 0,
@@ -233,6 +239,20 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
                   const ge_options* opt, int32_t num_sms,
                   int32_t* tile_m, int32_t* tile_n, int32_t* cta_group, int32_t* stages,
                   int64_t* num_tiles, int64_t* stream_k_tiles, int64_t* workspace_bytes, int32_t* split_k);
+
+/* The launch configuration ge_plan_ex reports (see ge_plan); swap_ab = 1 when the launch computes
+ * C^T = B^T A^T (tile_m / tile_n / num_tiles then describe the swapped problem: N x M). */
+typedef struct {
+    int32_t tile_m, tile_n, cta_group, stages;
+    int64_t num_tiles, stream_k_tiles, workspace_bytes;
+    int32_t split_k, multicast, swap_ab;
+} ge_plan_info;
+
+/* ge_plan with every planning decision, including multicast clusters and swap-AB (layouts and
+ * options matter: swap-AB depends on the bias mode and prologue; pass op through opt->... as for a
+ * launch; the op's bias flag is taken from `op`). */
+ge_status ge_plan_ex(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
+                     int32_t op, const ge_options* opt, int32_t num_sms, ge_plan_info* out);
 
 /* Number of fused kernels this library has launched in this process (for launch accounting). */
 uint64_t ge_launch_count(void);

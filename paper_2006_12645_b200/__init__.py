@@ -54,7 +54,14 @@ class GEOptions(ctypes.Structure):
                 ("cta_group", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_int64), ("multicast", ctypes.c_int32),
                 ("prologue_tile", ctypes.c_void_p), ("ld_prologue_tile", ctypes.c_int64),
-                ("stride_prologue_tile", ctypes.c_int64)]
+                ("stride_prologue_tile", ctypes.c_int64), ("swap_ab", ctypes.c_int32)]
+
+
+class GEPlanInfo(ctypes.Structure):
+    _fields_ = [("tile_m", ctypes.c_int32), ("tile_n", ctypes.c_int32), ("cta_group", ctypes.c_int32),
+                ("stages", ctypes.c_int32), ("num_tiles", ctypes.c_int64), ("stream_k_tiles", ctypes.c_int64),
+                ("workspace_bytes", ctypes.c_int64), ("split_k", ctypes.c_int32), ("multicast", ctypes.c_int32),
+                ("swap_ab", ctypes.c_int32)]
 
 
 class GEError(RuntimeError):
@@ -99,6 +106,8 @@ def load_library():
     lib.ge_plan.argtypes = [I64, I64, I64, I64, I32, I32, OPT, I32, ctypes.POINTER(I32), ctypes.POINTER(I32),
                             ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64),
                             ctypes.POINTER(I64), ctypes.POINTER(I32)]
+    lib.ge_plan_ex.restype = I32
+    lib.ge_plan_ex.argtypes = [I64, I64, I64, I64, I32, I32, I32, OPT, I32, ctypes.POINTER(GEPlanInfo)]
     lib.ge_launch_count.restype = ctypes.c_uint64
     lib.ge_launch_count.argtypes = []
     lib.ge_debug_read.restype = I32
@@ -158,12 +167,12 @@ _opt_cache = {}
 
 
 def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, stream_k=0, ws=None, multicast=0,
-             tile=None):
+             tile=None, swap_ab=0):
     """ge_options for these arguments; reused across calls with the same ones (per-call host cost).
     tile: (ptr, ld, batch stride) of the Hadamard prologue operand S."""
     key = (bias_mode, ldbias, prologue, scale.data_ptr() if scale is not None else 0, out_dtype, tile_n,
            cta_group, stream_k, ws.data_ptr() if ws is not None else 0, ws.numel() if ws is not None else 0,
-           multicast, tile)
+           multicast, tile, swap_ab)
     o = _opt_cache.get(key)
     if o is not None:
         return o
@@ -181,6 +190,7 @@ def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, s
     o.tile_n = int(tile_n)
     o.cta_group = int(cta_group)
     o.multicast = int(multicast)
+    o.swap_ab = int(swap_ab)
     if len(_opt_cache) > 512:
         _opt_cache.clear()
     _opt_cache[key] = o
@@ -300,7 +310,8 @@ def _bias_ld(bias, bias_mode):
 def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor] = None, *, op: Optional[str] = None,
                   bias_mode: str = "row", prologue: Optional[str] = None, scale: Optional[torch.Tensor] = None,
                   out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
-                  cta_group: int = 0, stream_k: int = 0, multicast: int = 0, stream=None) -> torch.Tensor:
+                  cta_group: int = 0, stream_k: int = 0, multicast: int = 0, swap_ab: int = 0,
+                  stream=None) -> torch.Tensor:
     """C = relu_add(prologue(A) @ B, bias) on the current CUDA device (fp16 in, fp32 accumulate).
 
     A: (M, K) fp16, B: (K, N) fp16, row- or column-major views.  bias: (N,) for bias_mode "row",
@@ -332,7 +343,7 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     ldbias, _ = _bias_ld(bias, bias_mode)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile, swap_ab)
     st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
                            bias.data_ptr() if bias is not None else None, out.data_ptr(), max(out.stride(0), N, 1),
                            _op(op, bias), ctypes.byref(o), sh)
@@ -343,7 +354,8 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
 def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.Tensor,
                    bias: Optional[torch.Tensor] = None, *, op: Optional[str] = None, bias_mode: str = "row",
                    out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
-                   cta_group: int = 0, stream_k: int = 0, multicast: int = 0, stream=None) -> torch.Tensor:
+                   cta_group: int = 0, stream_k: int = 0, multicast: int = 0, swap_ab: int = 0,
+                  stream=None) -> torch.Tensor:
     """Sum of matmuls (Listing 4): C = epilogue(A @ B + P @ Q) in one kernel, one TMEM
     accumulator.  A (M, K1), B (K1, N), P (M, K2), Q (K2, N); P must share A's layout (row/col
     major) and Q B's."""
@@ -367,7 +379,7 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
     ldbias, _ = _bias_ld(bias, bias_mode)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, None, None, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, None, swap_ab)
     st = lib.gemm2_epilogue(M, N, K1, K2, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb, P.data_ptr(), ldp,
                             Q.data_ptr(), ldq, bias.data_ptr() if bias is not None else None, out.data_ptr(),
                             max(out.stride(0), N, 1), _op(op, bias), ctypes.byref(o), sh)
@@ -396,7 +408,7 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
                           op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
                           scale: Optional[torch.Tensor] = None, out_dtype: torch.dtype = torch.float16,
                           out: Optional[torch.Tensor] = None, tile_n: int = 0, cta_group: int = 0,
-                          stream_k: int = 0, multicast: int = 0, stream=None) -> torch.Tensor:
+                          stream_k: int = 0, multicast: int = 0, swap_ab: int = 0, stream=None) -> torch.Tensor:
     """Strided-batched form: A (b, M, K), B (b, K, N), bias (N,)/(b, N) [row], (M,)/(b, M) [col],
     (M, ld)/(b, M, ld) [full]; a 1-D/2-D bias is shared by every item.  One persistent launch."""
     lib = load_library()
@@ -409,7 +421,7 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
         out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile, swap_ab)
     st = lib.gemm_epilogue_batched(batch, M, N, K, la, lb, A.data_ptr(), lda, sA, B.data_ptr(), ldb, sB,
                                    bias.data_ptr() if bias is not None else None, sbias, out.data_ptr(),
                                    max(out.stride(1), N, 1), out.stride(0), _op(op, bias), ctypes.byref(o), sh)
@@ -421,7 +433,7 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
                        op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
                        scale: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                        out_dtype: torch.dtype = torch.float16, tile_n: int = 0, cta_group: int = 0,
-                       stream_k: int = 0, multicast: int = 0, stream=None) -> torch.Tensor:
+                       stream_k: int = 0, multicast: int = 0, swap_ab: int = 0, stream=None) -> torch.Tensor:
     """End-to-end path through the C ABI with HOST (CPU, ideally pinned) tensors: the library copies
     the inputs to the device, runs the fused kernel and copies C back, synchronously."""
     lib = load_library()
@@ -438,7 +450,7 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
                           pin_memory=A.is_pinned())
     out3 = out if out.dim() == 3 else out.unsqueeze(0)
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k, multicast=multicast,
-                 tile=tile)
+                 tile=tile, swap_ab=swap_ab)
     st = lib.gemm_epilogue_host(batch, M, N, K, la, lb, A3.data_ptr(), lda, sA, B3.data_ptr(), ldb, sB,
                                 bias.data_ptr() if bias is not None else None, sbias, out3.data_ptr(),
                                 max(out3.stride(1), N, 1), out3.stride(0), _op(op, bias), ctypes.byref(o),
@@ -453,17 +465,18 @@ def validate_args(*args) -> int:
 
 
 def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: int = 148, tile_n: int = 0,
-         cta_group: int = 0, stream_k: int = 0, prologue: Optional[str] = None, multicast: int = 0) -> dict:
+         cta_group: int = 0, stream_k: int = 0, prologue: Optional[str] = None, multicast: int = 0,
+         swap_ab: int = 0, op: str = "bias_relu", bias_mode: str = "row") -> dict:
+    """The launch configuration the library's planner picks (ge_plan_ex), assuming a stream-K
+    workspace is passed (the device entry points of this binding always pass one)."""
     lib = load_library()
-    o = _options("row", 0, prologue, None, torch.float16, tile_n, cta_group, stream_k, multicast=multicast)
-    tm, tn, cg, stg, spl = (ctypes.c_int32() for _ in range(5))
-    nt, sk, wsb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-    st = lib.ge_plan(batch, M, N, K, 0 if layouts[0] == "r" else 1, 0 if layouts[1] == "r" else 1, ctypes.byref(o),
-                     num_sms, ctypes.byref(tm), ctypes.byref(tn), ctypes.byref(cg), ctypes.byref(stg),
-                     ctypes.byref(nt), ctypes.byref(sk), ctypes.byref(wsb), ctypes.byref(spl))
+    o = _options(bias_mode, 0, prologue, None, torch.float16, tile_n, cta_group, stream_k, multicast=multicast,
+                 swap_ab=swap_ab)
+    info = GEPlanInfo()
+    st = lib.ge_plan_ex(batch, M, N, K, 0 if layouts[0] == "r" else 1, 0 if layouts[1] == "r" else 1,
+                        _op(op, True), ctypes.byref(o), num_sms, ctypes.byref(info))
     _check(st)
-    return {"tile_m": tm.value, "tile_n": tn.value, "cta_group": cg.value, "stages": stg.value,
-            "num_tiles": nt.value, "stream_k_tiles": sk.value, "workspace_bytes": wsb.value, "split_k": spl.value}
+    return {f: getattr(info, f) for f, _ in GEPlanInfo._fields_}
 
 
 def launch_count() -> int:

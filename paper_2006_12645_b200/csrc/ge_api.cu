@@ -132,6 +132,7 @@ ge_status validate_options(const Args& a) {
     if (o.multicast == 2 && (o.prologue != GE_PRO_NONE || o.stream_k == 2 || (o.cta_group && o.cta_group != 2) ||
                              (o.tile_n && o.tile_n != 256 && o.tile_n != 512)))
         return fail(GE_ERR_INVALID_VALUE, "multicast = 2 needs no prologue, stream_k != 2, cta_group 0/2, tile_n 0/256/512");
+    if (o.swap_ab < 0 || o.swap_ab > 2) return fail(GE_ERR_INVALID_VALUE, "swap_ab must be 0, 1 or 2");
     if (o.workspace_bytes < 0 || (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 15)))
         return fail(GE_ERR_INVALID_VALUE, "workspace must be 16-byte aligned with a non-negative size");
     return GE_OK;
@@ -386,7 +387,8 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap, bool sk_allowed) {
             for (int64_t S = 2; S <= smax; ++S) {
                 const int64_t units = 4 * bn / 32;
                 const int64_t recv = cdiv(units, S) * (S - 1) * 32 * 32 * 4;
-                if (recv > static_cast<int64_t>(ge::stages_for(bn, 1)) * (128 + bn) * 64 * 2) continue;
+                if (recv > static_cast<int64_t>(ge::stages_for(bn, 1, a.o.prologue == GE_PRO_HADAMARD)) * (128 + bn) * 64 * 2)
+                    continue;
                 const int bi = bn == 64 ? 0 : bn == 128 ? 1 : bn == 192 ? 2 : 3;
                 // fallback (no device): cudaOccupancyMaxActiveClusters measured on B200, S = 2..8
                 static const int kCap148[9] = {0, 0, 74, 45, 33, 26, 22, 15, 15};
@@ -408,7 +410,8 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap, bool sk_allowed) {
         }
         if (a.o.multicast == 2) cost = 1e300;                      // forced multicast: pairs only below
         if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
-            best = Plan{bn, cg, ge::stages_for(bn, cg), false, tiles, sk, sk ? conc : std::min<int64_t>(tiles, conc)};
+            best = Plan{bn, cg, ge::stages_for(bn, cg, a.o.prologue == GE_PRO_HADAMARD), false, tiles, sk,
+                        sk ? conc : std::min<int64_t>(tiles, conc)};
             if (splits) {
                 best.splits = splits;
                 best.clusters = tiles * splits;
@@ -583,10 +586,54 @@ bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, i
     return true;
 }
 
+// Swap-AB: C^T = B^T A^T.  Legal where the epilogue commutes with the
+// transpose without new bias addressing (ROW <-> COL, no FULL bias), with no prologue on A (it would
+// become the MMA's B operand) and no sum of matmuls.  Heuristic: skinny M (<= 64) against a long N,
+// where the unswapped tile wastes most of every A stage on zero-filled rows and the 128-row MMA side
+// would hold only M valid rows (a shallow ring of useful B bytes, a split-K reduction of mostly zeros).
+bool swap_legal(const Args& a) {
+    return a.o.prologue == GE_PRO_NONE && a.K2 == 0 && !(has_bias(a.op) && a.o.bias_mode == GE_BIAS_FULL) &&
+           a.o.multicast != 2 && a.o.stream_k != 2 && a.o.cta_group != 2 && a.o.tile_n != 512;
+}
+bool use_swap(const Args& a) {
+    if (a.o.swap_ab == 1 || !swap_legal(a)) return false;
+    if (a.o.swap_ab == 2) return true;
+    return a.M <= 64 && a.N >= 1024 && !a.o.tile_n && !a.o.cta_group;
+}
+// The swapped problem: A' = B^T (M' = N), B' = A^T (N' = M); a transposed view flips the layout
+// bit and keeps the leading dimension; the bias modes ROW (bias[j]) and COL (bias[i]) trade places.
+Args swapped(const Args& a) {
+    Args t = a;
+    t.M = a.N;
+    t.N = a.M;
+    t.la = a.lb == GE_ROW_MAJOR ? GE_COL_MAJOR : GE_ROW_MAJOR;
+    t.lb = a.la == GE_ROW_MAJOR ? GE_COL_MAJOR : GE_ROW_MAJOR;
+    t.A = a.B;
+    t.lda = a.ldb;
+    t.sA = a.sB;
+    t.B = a.A;
+    t.ldb = a.lda;
+    t.sB = a.sA;
+    if (has_bias(a.op)) t.o.bias_mode = a.o.bias_mode == GE_BIAS_ROW ? GE_BIAS_COL : GE_BIAS_ROW;
+    return t;
+}
+
+ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans);
+
 ge_status launch(Args& a, cudaStream_t st) {
     ge_status s = validate(a);
     if (s != GE_OK) return s;
     if (a.batch == 0 || a.M == 0 || a.N == 0) return GE_OK;
+    if (use_swap(a)) {
+        Args t = swapped(a);
+        return launch_impl(t, st, true);
+    }
+    return launch_impl(a, st, false);
+}
+
+// Plan, encode and launch an already validated problem (c_trans: store C transposed, swap-AB).
+ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
+    ge_status s;
     int sms = 0;
     s = device_info(&sms);
     if (s != GE_OK) return s;
@@ -602,7 +649,8 @@ ge_status launch(Args& a, cudaStream_t st) {
     const bool arow = a.la == GE_ROW_MAJOR, brow = a.lb == GE_ROW_MAJOR;
     const bool a_mn = !arow, b_mn = brow;          // row-major A is K-major; row-major B is N(MN)-major
     const bool f32 = a.o.out_dtype == GE_OUT_F32;
-    const bool pro = a.o.prologue != GE_PRO_NONE;
+    // prologue kernel variant: 1 in-place op on A, 2 with the Hadamard S tile staged next to A
+    const int pro = a.o.prologue == GE_PRO_NONE ? 0 : a.o.prologue == GE_PRO_HADAMARD ? 2 : 1;
     const int es = f32 ? 4 : 2;
 
     ge::Maps maps;
@@ -618,6 +666,16 @@ ge_status launch(Args& a, cudaStream_t st) {
         else ok = encode3d(&maps.b, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.B, a.N, a.K, a.batch, a.ldb, a.sB, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for B");
     }
+    if (a.K > 0 && pro == 2) {
+        // Hadamard S: A's geometry and box (it lands at the same swizzled offsets as A); the P slot
+        const int64_t sT = a.batch > 1 ? a.o.stride_prologue_tile : 0;
+        bool ok;
+        if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.o.prologue_tile, a.K, a.M,
+                                 sT ? a.batch : 1, a.o.ld_prologue_tile, sT, 64, 128);
+        else ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.o.prologue_tile, a.M, a.K,
+                           sT ? a.batch : 1, a.o.ld_prologue_tile, sT, 64, 64);
+        if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the prologue tile");
+    }
     if (a.K2 > 0) {
         bool ok;
         if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.K2, a.M, 1, a.ldp, 0, 64, 128);
@@ -628,7 +686,7 @@ ge_status launch(Args& a, cudaStream_t st) {
         else ok = encode3d(&maps.q, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.Q, a.N, a.K2, 1, a.ldq, 0, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for Q");
     }
-    const bool c_tma = (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && ((a.ldc * es) % 16 == 0) &&
+    const bool c_tma = !c_trans && (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && ((a.ldc * es) % 16 == 0) &&
                        (a.batch == 1 || (a.sC * es) % 16 == 0);
     if (c_tma) {
         if (!encode3d(&maps.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, es, a.C, a.N,
@@ -670,18 +728,14 @@ ge_status launch(Args& a, cudaStream_t st) {
     p.scale = a.o.prologue == GE_PRO_SCALE_K ? a.o.prologue_scale : nullptr;
     p.prologue = a.o.prologue;
     p.scale_vec = p.scale && (reinterpret_cast<uintptr_t>(p.scale) % 16 == 0);
-    // the prologue kernels' transform warps load A (and S) themselves
-    p.a = static_cast<const __half*>(a.A);
-    p.lda = a.lda;
-    p.stride_a = a.sA;
-    p.s_tile = a.o.prologue == GE_PRO_HADAMARD ? static_cast<const __half*>(a.o.prologue_tile) : nullptr;
-    p.lds = a.o.ld_prologue_tile;
-    p.stride_s = a.o.stride_prologue_tile;
+    p.s_batched = (a.batch > 1 && a.o.stride_prologue_tile != 0) ? 1 : 0;
+
     p.C = a.C;
     p.ldc = a.ldc;
     p.stride_c = a.sC;
     p.c_tma = c_tma ? 1 : 0;
     p.c_vec = c_tma ? 1 : 0;                      // same alignment conditions as the TMA store
+    p.c_trans = c_trans ? 1 : 0;
 
 #if GE_DBG
     // diagnostics build only (libgemm_epilogue_dbg.so): counters and timing experiments
@@ -736,7 +790,7 @@ Args make_args(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t la, int32
                int64_t ldc, int64_t sC, int32_t op, const ge_options* opt) {
     Args a{batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op, {}};
     if (opt) a.o = *opt;
-    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0, nullptr, 0, 0};
+    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0, nullptr, 0, 0, 0};
     return a;
 }
 
@@ -782,20 +836,24 @@ int clusters_cg1(int bn, int cluster) {
     return bn == 64 ? clusters_cg1_bn64(cluster) : bn == 128 ? clusters_cg1_bn128(cluster)
          : bn == 192 ? clusters_cg1_bn192(cluster) : clusters_cg1_bn256(cluster);
 }
-int smem_bytes_for(int bn, int cg) {
+template <bool SX>
+int smem_bytes_t(int bn, int cg) {
     if (cg == 1)
-        return bn == 64 ? Cfg<64, 1>::kSmemBytes : bn == 128 ? Cfg<128, 1>::kSmemBytes
-             : bn == 192 ? Cfg<192, 1>::kSmemBytes : Cfg<256, 1>::kSmemBytes;
-    return bn == 128 ? Cfg<128, 2>::kSmemBytes : bn == 192 ? Cfg<192, 2>::kSmemBytes
-         : bn == 256 ? Cfg<256, 2>::kSmemBytes : Cfg<512, 2>::kSmemBytes;
+        return bn == 64 ? Cfg<64, 1, SX>::kSmemBytes : bn == 128 ? Cfg<128, 1, SX>::kSmemBytes
+             : bn == 192 ? Cfg<192, 1, SX>::kSmemBytes : Cfg<256, 1, SX>::kSmemBytes;
+    return bn == 128 ? Cfg<128, 2, SX>::kSmemBytes : bn == 192 ? Cfg<192, 2, SX>::kSmemBytes
+         : bn == 256 ? Cfg<256, 2, SX>::kSmemBytes : Cfg<512, 2, SX>::kSmemBytes;
 }
-int stages_for(int bn, int cg) {
+template <bool SX>
+int stages_t(int bn, int cg) {
     if (cg == 1)
-        return bn == 64 ? Cfg<64, 1>::kStages : bn == 128 ? Cfg<128, 1>::kStages
-             : bn == 192 ? Cfg<192, 1>::kStages : Cfg<256, 1>::kStages;
-    return bn == 128 ? Cfg<128, 2>::kStages : bn == 192 ? Cfg<192, 2>::kStages
-         : bn == 256 ? Cfg<256, 2>::kStages : Cfg<512, 2>::kStages;
+        return bn == 64 ? Cfg<64, 1, SX>::kStages : bn == 128 ? Cfg<128, 1, SX>::kStages
+             : bn == 192 ? Cfg<192, 1, SX>::kStages : Cfg<256, 1, SX>::kStages;
+    return bn == 128 ? Cfg<128, 2, SX>::kStages : bn == 192 ? Cfg<192, 2, SX>::kStages
+         : bn == 256 ? Cfg<256, 2, SX>::kStages : Cfg<512, 2, SX>::kStages;
 }
+int smem_bytes_for(int bn, int cg, bool sx) { return sx ? smem_bytes_t<true>(bn, cg) : smem_bytes_t<false>(bn, cg); }
+int stages_for(int bn, int cg, bool sx) { return sx ? stages_t<true>(bn, cg) : stages_t<false>(bn, cg); }
 }  // namespace ge
 
 extern "C" {
@@ -1057,6 +1115,33 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     if (stream_k_tiles) *stream_k_tiles = p.sk_tiles;
     if (workspace_bytes) *workspace_bytes = static_cast<int64_t>(sk_workspace_bytes(p));
     if (split_k) *split_k = p.splits > 1 ? p.splits : 1;
+    return GE_OK;
+}
+
+ge_status ge_plan_ex(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB, int32_t op,
+                     const ge_options* opt, int32_t num_sms, ge_plan_info* out) {
+    g_detail.clear();
+    Args a = make_args(batch, M, N, K, layoutA, layoutB, nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0, op,
+                       opt);
+    if (batch < 0 || M < 0 || N < 0 || K < 0 || num_sms <= 0 || !out) return fail(GE_ERR_INVALID_VALUE, "bad plan arguments");
+    if (!op_valid(op)) return fail(GE_ERR_INVALID_VALUE, "bad epilogue op (see ge_epilogue_op flags)");
+    {
+        const ge_status so = validate_options(a);
+        if (so != GE_OK) return so;
+    }
+    const bool sw = use_swap(a);
+    const Args t = sw ? swapped(a) : a;
+    const Plan p = make_plan(t, num_sms, split_capacity(), true);
+    out->tile_m = 128 * p.cg * (p.mc ? 2 : 1);
+    out->tile_n = p.bn;
+    out->cta_group = p.cg;
+    out->stages = p.stages;
+    out->num_tiles = p.tiles;
+    out->stream_k_tiles = p.sk_tiles;
+    out->workspace_bytes = static_cast<int64_t>(sk_workspace_bytes(p));
+    out->split_k = p.splits > 1 ? p.splits : 1;
+    out->multicast = p.mc ? 1 : 0;
+    out->swap_ab = sw ? 1 : 0;
     return GE_OK;
 }
 

@@ -61,6 +61,17 @@
 #ifndef GE_EPI_FAST
 #define GE_EPI_FAST 1
 #endif
+// The MMA warp polls its stage barriers without the try_wait suspend hint (a suspended warp wakes
+// some time after the phase completes; the tensor pipe idles meanwhile).
+#ifndef GE_MMA_SPIN
+#define GE_MMA_SPIN 0
+#endif
+// Paired acquire: the two k-blocks of a ring-slot pair land on ONE full barrier (the even slot's)
+// and the MMA warp waits once per pair (single-accumulator-half kernels without a prologue or
+// multicast); halves the per-k-block barrier round trips that bound narrow tiles.
+#ifndef GE_PAIR_ACQ
+#define GE_PAIR_ACQ 0
+#endif
 
 namespace ge {
 
@@ -68,7 +79,7 @@ constexpr int kBK = 64;                 // K per pipeline stage (64 fp16 = one 1
 constexpr int kUmmaK = 16;              // K per tcgen05.mma for 16-bit inputs
 constexpr int kRowsPerCta = 128;        // accumulator rows per CTA (= TMEM lanes)
 constexpr int kSmemBudget = 232448;     // 227 KB dynamic smem per CTA on sm_100
-constexpr int kXformWarps = 4;
+constexpr int kXformWarps = 4;     // prologue transform warps (PRO kernels)
 constexpr int kStagingSetBytes = 16384; // one staging buffer per epilogue warp: 8 x 2 KB (fp16) or 4 x 4 KB (fp32)
 
 enum : int { BIAS_NONE = -1, BIAS_ROW = 0, BIAS_COL = 1, BIAS_FULL = 2 };
@@ -89,22 +100,19 @@ struct Params {
     int act;                        // ACT_* applied at the root of the epilogue
     float bias_sign;                // +1 add, -1 subtract the bias
     int literal;                    // paper-literal rounding point (DESIGN.md R-C3): fp16(fp16(acc) +- bias)
-    // prologue (PRO kernels): the transform warps read A from global memory themselves (A is not
-    // TMA-loaded), apply the op in registers and store the swizzled stage: "performed during the
-    // data movement", PAPER.md:1215-1231 (one smem write per element instead of TMA write + read +
-    // write back)
+    // prologue (PRO kernels): the TMA lands the A stage (and, for HADAMARD, the S stage) and the
+    // transform warps rewrite A in place in smem before the MMA reads it
     const float* scale;             // SCALE_K: s[k], fp32
     int prologue;                   // PRO_*
     int scale_vec;
-    const __half* a;                // A (logical M x K, layout of the kernel's A_MN), leading dim, batch stride
-    long long lda, stride_a;
-    const __half* s_tile;           // HADAMARD: S, same layout as A (M x K fp16), leading dim, batch stride
-    long long lds, stride_s;
+    int s_batched;                  // HADAMARD: 1 = one S per batch item, 0 = one S shared by all items
     // output
     void* C;
     long long ldc, stride_c;
     int c_tma;                      // 1: TMA store; 0: st.global path
     int c_vec;                      // st.global path may use 16-B vector stores (aligned rows)
+    int c_trans;                    // swap-AB launch: the kernel computes
+                                    // C^T = B^T A^T, so element (row, col) goes to C[col * ldc + row]
     // L2 eviction priority of the operand loads / output stores (0 normal, 1 first, 2 last)
     int hint_a, hint_b, hint_c;
     // stream-K: tiles [dp_tiles, num_tiles) are split into sk_units
@@ -140,7 +148,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-template <int BN, int CG>
+// SX: the Hadamard prologue's S tile is staged like A (same box, same swizzle) in its own ring slot.
+template <int BN, int CG, bool SX = false>
 struct Cfg {
     static constexpr int kTileM = kRowsPerCta * CG;
     static constexpr int kUmmaN = BN < 256 ? BN : 256;                // N of one tcgen05.mma
@@ -150,7 +159,8 @@ struct Cfg {
     static constexpr int kBRows = BN / CG;                            // B rows (N) staged per CTA
     static constexpr int kAStage = kRowsPerCta * kBK * 2;             // 16 KB
     static constexpr int kBStage = kBRows * kBK * 2;
-    static constexpr int kStageBytes = kAStage + kBStage;
+    static constexpr int kSStage = SX ? kAStage : 0;
+    static constexpr int kStageBytes = kAStage + kBStage + kSStage;
     static constexpr int kBarBytes = 320;                             // (3S + 8) mbarriers + TMEM slot
     // Epilogue staging buffers per warp (double-buffered TMA stores).
     static constexpr int kStagingBufs = 2;
@@ -299,19 +309,22 @@ __host__ __device__ constexpr int kernel_threads(bool out_f32, bool pro) {
 // MC: clusters of two CTA pairs stacked along M that share the B tile: each CTA loads half of its
 // B block and multicasts it to the CTA at the same position in the other pair (a third less L2->SM
 // operand traffic per flop); data-parallel tiles only (no prologue, stream-K or split-K).
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG, bool MC = false>
-__global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO), 1)
+// PRO: 0 no prologue; 1 in-place prologue op on the A stage (SCALE_K / RELU); 2 the same with the
+// Hadamard tile S staged by TMA next to A (its second input dataspace).
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, int PRO, int CG, bool MC = false>
+__global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO != 0), 1)
 ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_p,
                 const __grid_constant__ CUtensorMap tmap_q, const Params p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-    using C_ = Cfg<BN, CG>;
+    using C_ = Cfg<BN, CG, PRO == 2>;
     constexpr int S = C_::kStages;
     constexpr int W = 32;                                // output columns per epilogue chunk (one tcgen05.ld)
     constexpr int NCHUNK = BN / W;
-    constexpr int EPI_WARPS = epi_warps(OUT_F32, PRO);
+    constexpr int EPI_WARPS = epi_warps(OUT_F32, PRO != 0);
     constexpr int NH = C_::kNHalves;
     constexpr int HALF_COLS = BN / NH;
+    constexpr bool kPairAcq = GE_PAIR_ACQ && !PRO && NH == 1 && !MC && GE_PAIR_RELEASE;
     constexpr uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, C_::kUmmaN, A_MN, B_MN);
 
     const unsigned long long g_entry = GE_DBG ? globaltimer() : 0ull;
@@ -321,7 +334,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* smem_a = smem;
     uint8_t* smem_b = smem + S * C_::kAStage;
-    uint8_t* smem_c = smem_b + S * C_::kBStage;
+    uint8_t* smem_s = smem_b + S * C_::kBStage;         // Hadamard S stages (PRO == 2 only)
+    uint8_t* smem_c = smem_s + S * C_::kSStage;
     __half* smem_bias = reinterpret_cast<__half*>(smem_c + C_::kStagingBytes);
     float* smem_bias_f = reinterpret_cast<float*>(smem_c + C_::kStagingBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_c + C_::kStagingBytes + C_::kBiasBytes);
@@ -353,6 +367,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             ptx::tma_prefetch(&tmap_p);
             ptx::tma_prefetch(&tmap_q);
         }
+        if (PRO == 2) ptx::tma_prefetch(&tmap_p);      // Hadamard S (the P slot: no sum of matmuls here)
         if (p.c_tma) ptx::tma_prefetch(&tmap_c);
     }
     if (warp == 1 && lane == 0) {
@@ -415,6 +430,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     // commit covers the even stage's MMAs too), so wait once per pair on it
                     if (!GE_PAIR_RELEASE) ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
                     else if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                    // paired acquire: both slots of a pair signal the even slot's full barrier, armed
+                    // once for the pair's bytes; a piece with an odd k-block count ends on a single
+                    // (the odd slot is skipped, MMA and producer agree on the rule)
+                    const bool pair_two = kPairAcq && (s & 1) == 0 && kb + 1 < pc.kb1;
+                    uint64_t* const fb = kPairAcq ? &full_bar[s & ~1] : &full_bar[s];
+                    const bool arm = !kPairAcq || (s & 1) == 0;
+                    const uint32_t n_sub = pair_two ? 2u : 1u;
                     // sum of matmuls (Listing 4): k-blocks past A.B's come from P.Q, same accumulator
                     const bool second = kb >= p.num_k_blocks1;
                     const CUtensorMap* map_a = second ? &tmap_p : &tmap_a;
@@ -428,29 +450,31 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (++s == S) { s = 0; phase ^= 1; }
                         continue;
                     }
-                    // PRO kernels: the transform warps write the A stage; the TMA brings B only
-                    constexpr uint32_t kTx = PRO ? C_::kBStage : C_::kStageBytes;
-                    if constexpr (CG == 2) {
+                    if constexpr (CG == 2 && !PRO) {
                         // The peer's bytes can only land after the leader's barrier entered this
                         // phase (the peer first waits on its empty[s], released by the MMA that
                         // consumed the previous phase), so a transiently negative tx-count is safe.
-                        if (leader) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * kTx);
+                        if (leader && arm) ptx::mbar_arrive_expect_tx(fb, 2 * n_sub * C_::kStageBytes);
                     } else {
-                        ptx::mbar_arrive_expect_tx(&full_bar[s], kTx);
+                        // single CTAs, and every CTA of a prologue pair: its own transform warps wait
+                        // for its own stage
+                        if (arm) ptx::mbar_arrive_expect_tx(fb, n_sub * C_::kStageBytes);
                     }
-                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol) {
-                        if constexpr (CG == 2) ptx::tma_load_3d_pair(dst, map, &full_bar[s], c0, c1, b, pol);
-                        else ptx::tma_load_3d(dst, map, &full_bar[s], c0, c1, b, pol);
+                    auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol, int cb) {
+                        if constexpr (CG == 2 && !PRO) ptx::tma_load_3d_pair(dst, map, fb, c0, c1, cb, pol);
+                        else ptx::tma_load_3d(dst, map, fb, c0, c1, cb, pol);
                     };
-                    if constexpr (PRO) {
-                        (void)sa;
-                        (void)pol_a;
-                    } else if constexpr (A_MN) {
+                    // A, and the Hadamard tile S with A's box and swizzle (element-aligned with A in smem)
+                    auto load_a = [&](uint8_t* dst, const CUtensorMap* map, int cb) {
+                        if constexpr (A_MN) {
 #pragma unroll
-                        for (int i = 0; i < kRowsPerCta / 64; ++i) load(sa + i * 8192, map_a, m0 + i * 64, k0, pol_a);
-                    } else {
-                        load(sa, map_a, k0, m0, pol_a);
-                    }
+                            for (int i = 0; i < kRowsPerCta / 64; ++i) load(dst + i * 8192, map, m0 + i * 64, k0, pol_a, cb);
+                        } else {
+                            load(dst, map, k0, m0, pol_a, cb);
+                        }
+                    };
+                    load_a(sa, map_a, b);
+                    if constexpr (PRO == 2) load_a(smem_s + s * C_::kSStage, &tmap_p, p.s_batched ? b : 0);
 #pragma unroll
                     for (int h = 0; h < NH; ++h) {
                         uint8_t* sbh = sb + h * C_::kBBlockBytes;
@@ -468,11 +492,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         } else if constexpr (B_MN) {
 #pragma unroll
                             for (int i = 0; i < C_::kBBlockRows / 64; ++i)
-                                load(sbh + i * 8192, map_b, nh + i * 64, k0, pol_b);
+                                load(sbh + i * 8192, map_b, nh + i * 64, k0, pol_b, b);
                         } else {
-                            load(sbh, map_b, k0, nh, pol_b);
+                            load(sbh, map_b, k0, nh, pol_b, b);
                         }
                     }
+                    if (kPairAcq && (s & 1) == 0 && !pair_two) ++s;   // single at the end of a piece
                     if (++s == S) { s = 0; phase ^= 1; }
                 }
             }
@@ -484,11 +509,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // in uniform registers); one elected lane issues each tcgen05 instruction.  The tensor
             // pipe queues only about one MMA, so the code between consecutive MMAs (barrier wait,
             // fence, commit) is kept minimal: it shows up directly as tensor idle time.
-            // stage s is ready when its TMA bytes landed (full) and, with a prologue, when the
-            // transform warps of both CTAs stored its A (xform)
+            // stage s is ready when its TMA bytes landed (full) or, with a prologue, when the
+            // transform warps of every CTA of the pair rewrote its A in place (xform)
             auto wait_ready = [&](int st, uint32_t ph, unsigned long long& acc) {
-                ptx::mbar_wait_timed(&full_bar[st], ph, dbg && lane == 0, acc);
-                if constexpr (PRO) ptx::mbar_wait_timed(&xform_bar[st], ph, dbg && lane == 0, acc);
+                uint64_t* bar = PRO ? &xform_bar[st] : &full_bar[st];
+                if (GE_MMA_SPIN && !dbg) ptx::mbar_wait_spin(bar, ph);
+                else ptx::mbar_wait_timed(bar, ph, dbg && lane == 0, acc);
             };
             const uint32_t a_base = ptx::smem_u32(smem_a);
             const uint32_t b_base = ptx::smem_u32(smem_b);
@@ -577,6 +603,25 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         }
                     }
                     ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
+                } else if constexpr (kPairAcq) {
+                    // paired acquire: one barrier wait and one commit per ring-slot pair
+                    for (int kb = pc.kb0; kb < pc.kb1;) {
+                        const bool two = kb + 1 < pc.kb1;
+                        wait_ready(s, phase, dl[DBG_MMA_FULL]);
+                        ptx::tc_fence_after();
+                        if (kb == pc.kb0) {
+                            ptx::mbar_wait_timed(&tempty_bar[acc], acc_phase ^ 1,
+                                                 dbg && lane == 0, dl[DBG_MMA_TEMPTY]);
+                            ptx::tc_fence_after();
+                        }
+                        mma_half(s, kb, 0);
+                        if (two) mma_half(s + 1, kb + 1, 0);
+                        ptx::mma_commit_elect<CG>(&empty_bar[s + 1], 0x3);   // frees both slots
+                        kb += two ? 2 : 1;
+                        if (kb == pc.kb1) ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
+                        s += 2;
+                        if (s == S) { s = 0; phase ^= 1; }
+                    }
                 } else {
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                         if (!(GE_EARLY_TEST && next_ready)) wait_ready(s, phase, dl[DBG_MMA_FULL]);
@@ -591,8 +636,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             // readiness of the next stage, tested before this stage's MMAs are issued
                             // so the barrier round trip overlaps the issue
                             const int sn = s + 1 == S ? 0 : s + 1;
-                            next_ready = ptx::mbar_test(&full_bar[sn], s + 1 == S ? phase ^ 1 : phase) &&
-                                         (!PRO || ptx::mbar_test(&xform_bar[sn], s + 1 == S ? phase ^ 1 : phase));
+                            next_ready = ptx::mbar_test(PRO ? &xform_bar[sn] : &full_bar[sn], s + 1 == S ? phase ^ 1 : phase);
                         }
                         mma_half(s, kb, 0);
                         release_stage(s);                         // smem slot free once these MMAs finish
@@ -844,7 +888,25 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     // st.global path: C whose base/ldc breaks the TMA alignment rules (scalar stores),
                     // or 16-B aligned rows written straight from registers (c_vec)
                     const long long off = static_cast<long long>(b) * p.stride_c + static_cast<long long>(row) * p.ldc;
-                    if (p.c_vec && col0 + W <= p.N) {
+                    if (p.c_trans) {
+                        // swap-AB: this thread's row is a column of C; the 32 lanes of the warp hold
+                        // 32 consecutive C columns, so each store instruction writes one contiguous
+                        // 64-B (fp16) / 128-B (fp32) segment of a C row
+                        const long long cb = static_cast<long long>(b) * p.stride_c + row;
+                        if constexpr (OUT_F32) {
+#pragma unroll
+                            for (int e = 0; e < W; ++e)
+                                if (col0 + e < p.N)
+                                    reinterpret_cast<float*>(p.C)[cb + static_cast<long long>(col0 + e) * p.ldc] =
+                                        __uint_as_float(w[e]);
+                        } else {
+                            const __half* hv = reinterpret_cast<const __half*>(w);
+#pragma unroll
+                            for (int e = 0; e < W; ++e)
+                                if (col0 + e < p.N)
+                                    reinterpret_cast<__half*>(p.C)[cb + static_cast<long long>(col0 + e) * p.ldc] = hv[e];
+                        }
+                    } else if (p.c_vec && col0 + W <= p.N) {
                         uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.C) + (off + col0) * ES);
 #pragma unroll
                         for (int g = 0; g < NV; ++g) dst[g] = make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
@@ -1102,103 +1164,81 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             dl[DBG_G_EPI_END] = globaltimer();
         }
     } else if (PRO && warp >= 4 + EPI_WARPS) {
-        // ===================== prologue: A global -> registers -> op -> swizzled smem stage ===========
-        // Sec. VII-C: the pointwise op is applied while A moves from global to
-        // shared memory, on register-staged data (the paper's Volta copy path), so the
-        // stage costs ONE smem write per element (a TMA load + in-place rewrite costs three).  The
-        // warps run ahead of the MMA by the ring depth; loads for the next k-block are issued as soon
-        // as the current one is stored, so their latency overlaps the wait for the next free slot.
-        //  K-major stage (A row-major; 128 rows x 128 B, 128-B swizzle): thread xt owns the logical
-        //   k-chunk c = xt % 8 of rows r_i = xt / 8 + 16 i (i < 8), stored at r_i * 128 +
-        //   ((c ^ (r_i % 8)) * 16): its 8 chunks share one 8-wide k range (one set of scale values);
-        //   a warp stores 4 whole 128-B rows (conflict-free) and loads 4 whole 128-B row segments.
-        //  MN-major stage (A col-major; two 64-m atoms of 64 k-rows x 128 B): thread xt owns the
-        //   m-chunk c = xt % 16 (atom c / 8) of k-rows k_i = xt / 16 + 8 i, stored at
-        //   (c / 8) * 8192 + k_i * 128 + (((c % 8) ^ (k_i % 8)) * 16).
-        // Out-of-range rows / k (tile tails) are zero-filled like the TMA path (the K tail adds 0).
+        // ===================== prologue transform of the A stage (in place, in smem) ==========
+        // (Sec. VII-C.)  The TMA lands A (and S) in the swizzled stage; these warps
+        // rewrite A in place and hand the stage to the MMA.  Measured alternative (round 2, DESIGN.md
+        // "Prologue"): loading A through registers (ld.global -> op -> st.shared, the paper's Volta copy
+        // path) saves two smem passes but its global loads could not be kept in flight deep enough
+        // (2-4x slower at 4096^3), so the TMA stays the loader.
         const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
-        constexpr int NCH = C_::kAStage / 16 / 128;          // 8 chunks of 16 B per thread
-        const int op = p.prologue;
-        const bool had = op == PRO_HADAMARD;
-        uint4 xa[NCH], xs[NCH];                               // A (and S) chunks of the next k-block
-        float sc[NCH];                                        // SCALE_K factors of those chunks
-        // 8 consecutive fp16 of row-major / col-major storage at element offset `off` of base, the
-        // first `valid` of them in range (0..8); 16-B aligned when valid == 8
-        auto ld8 = [&](const __half* base, long long off, int valid) -> uint4 {
-            if (valid >= 8) return __ldg(reinterpret_cast<const uint4*>(base + off));
-            uint4 r = make_uint4(0u, 0u, 0u, 0u);
-            __half* h = reinterpret_cast<__half*>(&r);
-            for (int e = 0; e < valid; ++e) h[e] = base[off + e];
-            return r;
-        };
-        int wi_l = 0, kb_l = 0;                               // the k-block the registers hold
-        auto load = [&](int wi, int kb) {
-            const Piece pc = work.get(wi);
-            int b, mt, nt;
-            decode_tile(p, pc.tile, TILE_M, b, mt, nt);
-            const int m0 = mt * TILE_M + rank * kRowsPerCta;
+        // Thread xt rewrites the 16-B chunks o = (i*128 + xt)*16, i = 0..7, of each 16 KB A stage.
+        //  K-major stage (row = m, 128-B rows of 64 k, 128-B swizzle): the logical k-chunk of all
+        //   eight chunks is kc = (xt % 8) ^ ((xt / 8) % 8), so the thread needs scale[k0+8kc .. +8];
+        //  MN-major stage (row = k, 64-m atoms of 8 KB): chunk i lies on k = k0 + (16i + xt/8) % 64.
+        // The 8 scale values of the NEXT k-block are prefetched while the current one is
+        // transformed (the scale vector would otherwise cost an L2 round trip per chunk).
+        const bool scale_k = p.prologue == PRO_SCALE_K;
+        const int kc = (xt & 7) ^ ((xt >> 3) & 7);
+        auto fetch = [&](int kb, float* dst) {
             const int k0 = kb * kBK;
-            const __half* A = p.a + static_cast<long long>(b) * p.stride_a;
-            const __half* Sm = had ? p.s_tile + static_cast<long long>(b) * p.stride_s : nullptr;
-            if constexpr (!A_MN) {
-                const int k = k0 + (xt & 7) * 8;
-                const int kv = max(0, min(8, p.K - k));
+            if constexpr (A_MN) {
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) {
-                    const int m = m0 + (xt >> 3) + 16 * i;
-                    const int v = m < p.M ? kv : 0;
-                    xa[i] = ld8(A, static_cast<long long>(m) * p.lda + k, v);
-                    if (had) xs[i] = ld8(Sm, static_cast<long long>(m) * p.lds + k, v);
-                }
-                if (op == PRO_SCALE_K) {
-                    if (p.scale_vec && kv == 8) {
-                        const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + k));
-                        const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + k + 4));
-                        sc[0] = s0.x; sc[1] = s0.y; sc[2] = s0.z; sc[3] = s0.w;
-                        sc[4] = s1.x; sc[5] = s1.y; sc[6] = s1.z; sc[7] = s1.w;
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) sc[e] = e < kv ? __ldg(p.scale + k + e) : 0.0f;
-                    }
+                for (int i = 0; i < 8; ++i) {
+                    const int k = k0 + ((i * 16 + (xt >> 3)) & 63);
+                    dst[i] = k < p.K ? __ldg(p.scale + k) : 0.0f;
                 }
             } else {
-                const int m = m0 + (xt & 15) * 8;
-                const int mv = max(0, min(8, p.M - m));
+                const int k = k0 + kc * 8;
+                if (p.scale_vec && k + 8 <= p.K) {
+                    const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + k));
+                    const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + k + 4));
+                    dst[0] = s0.x; dst[1] = s0.y; dst[2] = s0.z; dst[3] = s0.w;
+                    dst[4] = s1.x; dst[5] = s1.y; dst[6] = s1.z; dst[7] = s1.w;
+                } else {
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) {
-                    const int k = k0 + (xt >> 4) + 8 * i;
-                    const int v = k < p.K ? mv : 0;
-                    xa[i] = ld8(A, static_cast<long long>(k) * p.lda + m, v);
-                    if (had) xs[i] = ld8(Sm, static_cast<long long>(k) * p.lds + m, v);
-                    if (op == PRO_SCALE_K) sc[i] = k < p.K ? __ldg(p.scale + k) : 0.0f;
+                    for (int e = 0; e < 8; ++e) dst[e] = (k + e < p.K) ? __ldg(p.scale + k + e) : 0.0f;
                 }
             }
-            wi_l = wi;
-            kb_l = kb;
         };
-        auto advance = [&](int& wi, int& kb) {           // next k-block in the work sequence
-            if (++kb == work.get(wi).kb1) {
-                ++wi;
-                kb = (wi < work.count()) ? work.get(wi).kb0 : 0;
-            }
-        };
+        float sc_cur[8], sc_nxt[8];
+        if (scale_k && nkb > 0 && work.count() > 0) fetch(work.get(0).kb0, sc_nxt);
         int s = 0;
         uint32_t phase = 0;
-        if (nkb > 0 && work.count() > 0) {
-            int wi = 0, kb = work.get(0).kb0;
-            load(wi, kb);
-            while (wi < work.count()) {
-                // the slot is free once the MMAs that read its previous contents completed (paired
-                // release: the odd stage's commit covers the even one, as for the TMA producer)
-                if (!GE_PAIR_RELEASE) ptx::mbar_wait(&empty_bar[s], phase ^ 1);
-                else if ((s & 1) == 0) ptx::mbar_wait(&empty_bar[s + 1], phase ^ 1);
-                uint4 y[NCH];
+        for (int wi = 0; wi < work.count(); ++wi) {
+            const Piece pc = work.get(wi);
+            for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
+                if (scale_k) {
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) {
-                    y[i] = xa[i];
-                    uint32_t* w = reinterpret_cast<uint32_t*>(&y[i]);
-                    if (op == PRO_RELU) {
-                        // a' = max(a, +0): clear every lane with the sign bit set (exact, -0 -> +0)
+                    for (int e = 0; e < 8; ++e) sc_cur[e] = sc_nxt[e];
+                    int kn = kb + 1;                                  // next k-block this thread transforms
+                    if (kn == pc.kb1) kn = (wi + 1 < work.count()) ? work.get(wi + 1).kb0 : 0;
+                    fetch(kn, sc_nxt);                                // in flight during this stage
+                }
+                ptx::mbar_wait(&full_bar[s], phase);
+                uint8_t* sa = smem_a + s * C_::kAStage;
+                constexpr int NCH = C_::kAStage / 16 / 128;          // 8 chunks per thread
+                uint4 x[NCH];
+#pragma unroll
+                for (int i = 0; i < NCH; ++i) x[i] = *reinterpret_cast<const uint4*>(sa + (i * 128 + xt) * 16);
+                if constexpr (PRO == 2) {
+                    // HADAMARD: a' = RNE_fp16(s(i,k) * a(i,k)); S sits at the same swizzled offsets as A
+                    // (same box, same swizzle), and the fp16 x fp16 product is exact before its one
+                    // rounding (mul.rn.f16x2; DESIGN.md R-C18)
+                    const uint8_t* ss = smem_s + s * C_::kSStage;
+#pragma unroll
+                    for (int i = 0; i < NCH; ++i) {
+                        const uint4 y = *reinterpret_cast<const uint4*>(ss + (i * 128 + xt) * 16);
+                        __half2* h2 = reinterpret_cast<__half2*>(&x[i]);
+                        const __half2* s2 = reinterpret_cast<const __half2*>(&y);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) h2[e] = __hmul2(h2[e], s2[e]);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < NCH && PRO == 1; ++i) {
+                    if (!scale_k) {
+                        // RELU: a' = max(a, +0): clear every lane with the sign bit set (exact, -0 -> +0)
+                        uint32_t* w = reinterpret_cast<uint32_t*>(&x[i]);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             uint32_t u = w[e];
@@ -1206,55 +1246,29 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             if (u & 0x80000000u) u &= 0x0000FFFFu;
                             w[e] = u;
                         }
-                    } else if (op == PRO_SCALE_K) {
-                        // a' = RNE_fp16(s_k * a) (DESIGN.md R-C12)
-                        __half2* h2 = reinterpret_cast<__half2*>(&y[i]);
+                    } else {
+                        // SCALE_K: a' = RNE_fp16(s_k * a) (DESIGN.md R-C12)
+                        __half2* h2 = reinterpret_cast<__half2*>(&x[i]);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const float2 a = __half22float2(h2[e]);
-                            const float s0 = A_MN ? sc[i] : sc[2 * e];
-                            const float s1 = A_MN ? sc[i] : sc[2 * e + 1];
+                            const float s0 = A_MN ? sc_cur[i] : sc_cur[2 * e];
+                            const float s1 = A_MN ? sc_cur[i] : sc_cur[2 * e + 1];
                             h2[e] = __floats2half2_rn(s0 * a.x, s1 * a.y);
                         }
-                    } else if (had) {
-                        // a' = RNE_fp16(s(i,k) * a(i,k)): the fp16 x fp16 product is exact before its
-                        // one rounding (mul.rn.f16x2; DESIGN.md R-C18)
-                        __half2* h2 = reinterpret_cast<__half2*>(&y[i]);
-                        const __half2* s2 = reinterpret_cast<const __half2*>(&xs[i]);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) h2[e] = __hmul2(h2[e], s2[e]);
                     }
                 }
-                // registers are free again: issue the next k-block's loads before storing this one
-                int wn = wi, kn = kb;
-                advance(wn, kn);
-                if (wn < work.count()) load(wn, kn);
-                uint8_t* sa = smem_a + s * C_::kAStage;
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) {
-                    int off;
-                    if constexpr (!A_MN) {
-                        const int r = (xt >> 3) + 16 * i;
-                        off = r * 128 + (((xt & 7) ^ (r & 7)) * 16);
-                    } else {
-                        const int c = xt & 15, kk = (xt >> 4) + 8 * i;
-                        off = (c >> 3) * 8192 + kk * 128 + ((((c & 7) ^ (kk & 7))) * 16);
-                    }
-                    *reinterpret_cast<uint4*>(sa + off) = y[i];
-                }
-                ptx::fence_proxy_async_smem();               // generic-proxy stores -> the MMA (async proxy)
+                for (int i = 0; i < NCH; ++i) *reinterpret_cast<uint4*>(sa + (i * 128 + xt) * 16) = x[i];
+                ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
                     if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&xform_bar[s], 0);
                     else ptx::mbar_arrive(&xform_bar[s]);
                 }
                 if (++s == S) { s = 0; phase ^= 1; }
-                wi = wn;
-                kb = kn;
             }
         }
-        (void)wi_l;
-        (void)kb_l;
     }
 
     // ---- teardown: every role done; the allocating warp frees TMEM

@@ -14,14 +14,15 @@ struct Maps {
     CUtensorMap a, b, c, p, q;      // p, q: second matmul of a sum of matmuls (unused otherwise)
 };
 
-// Smem bytes the (BN, CG) configuration requests (host and device agree through Cfg).
-int smem_bytes_for(int bn, int cg);
-int stages_for(int bn, int cg);
+// Smem bytes / ring stages of the (BN, CG) configuration, sx: with the Hadamard S stage (host and
+// device agree through Cfg).
+int smem_bytes_for(int bn, int cg, bool sx = false);
+int stages_for(int bn, int cg, bool sx = false);
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool PRO, int CG, bool MC = false>
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, int PRO, int CG, bool MC = false>
 cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st) {
     auto kern = ge_fused_kernel<BN, A_MN, B_MN, OUT_F32, PRO, CG, MC>;
-    constexpr int smem = Cfg<BN, CG>::kSmemBytes;
+    constexpr int smem = Cfg<BN, CG, PRO == 2>::kSmemBytes;
     static bool attr_done = false;   // benign race: setting the attribute twice is harmless
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -30,7 +31,7 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(kernel_threads(OUT_F32, PRO), 1, 1);
+    cfg.blockDim = dim3(kernel_threads(OUT_F32, PRO != 0), 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -57,7 +58,7 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
 // query fails); the split-K planner uses it (cluster scheduling is GPC-bound, not SM-count-bound).
 template <int BN, int CG, bool MC = false>
 int max_active_clusters(int cluster) {
-    auto kern = ge_fused_kernel<BN, false, false, false, false, CG, MC>;
+    auto kern = ge_fused_kernel<BN, false, false, false, 0, CG, MC>;
     constexpr int smem = Cfg<BN, CG>::kSmemBytes;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
@@ -82,55 +83,49 @@ int max_active_clusters(int cluster) {
     return n;
 }
 
-// Dispatch over the 16 (A_MN, B_MN, OUT_F32, PRO) variants of one (BN, CG) configuration.
+// Dispatch over the 24 (A_MN, B_MN, OUT_F32, PRO in {0, 1, 2}) variants of one (BN, CG) configuration.
 template <int BN, int CG, bool MC = false>
-cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, bool pro, const Maps& m, const Params& p, int grid,
+cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, int pro, const Maps& m, const Params& p, int grid,
                          cudaStream_t st) {
-    const int key = (a_mn ? 8 : 0) | (b_mn ? 4 : 0) | (f32 ? 2 : 0) | (pro ? 1 : 0);
-    switch (key) {
+    const int key = (a_mn ? 4 : 0) | (b_mn ? 2 : 0) | (f32 ? 1 : 0);
+    switch (key * 3 + pro) {
 // (BN = 192 with CTA pairs stages 96 B rows per CTA: only K-major B, whose TMA box takes any row
 // count; an MN-major B stage is built from 64-column swizzle atoms.)
 #define GE_CASE(K, AM, BM, F, P)                                                  \
-    case K:                                                                       \
+    case K * 3 + P:                                                               \
         if constexpr ((BM && BN == 192 && CG == 2) || (MC && P)) return cudaErrorInvalidValue; \
         else return launch_one<BN, AM, BM, F, P, CG, MC>(m, p, grid, st);
-        GE_CASE(0, false, false, false, false)
-        GE_CASE(1, false, false, false, true)
-        GE_CASE(2, false, false, true, false)
-        GE_CASE(3, false, false, true, true)
-        GE_CASE(4, false, true, false, false)
-        GE_CASE(5, false, true, false, true)
-        GE_CASE(6, false, true, true, false)
-        GE_CASE(7, false, true, true, true)
-        GE_CASE(8, true, false, false, false)
-        GE_CASE(9, true, false, false, true)
-        GE_CASE(10, true, false, true, false)
-        GE_CASE(11, true, false, true, true)
-        GE_CASE(12, true, true, false, false)
-        GE_CASE(13, true, true, false, true)
-        GE_CASE(14, true, true, true, false)
-        GE_CASE(15, true, true, true, true)
+#define GE_CASES(K, AM, BM, F) GE_CASE(K, AM, BM, F, 0) GE_CASE(K, AM, BM, F, 1) GE_CASE(K, AM, BM, F, 2)
+        GE_CASES(0, false, false, false)
+        GE_CASES(1, false, false, true)
+        GE_CASES(2, false, true, false)
+        GE_CASES(3, false, true, true)
+        GE_CASES(4, true, false, false)
+        GE_CASES(5, true, false, true)
+        GE_CASES(6, true, true, false)
+        GE_CASES(7, true, true, true)
+#undef GE_CASES
 #undef GE_CASE
     }
     return cudaErrorInvalidValue;
 }
 
 // Defined in ge_inst_*.cu (one translation unit per configuration, compiled in parallel).
-cudaError_t launch_cg1_bn64(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg1_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg1_bn192(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn192(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn64(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn128(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn192(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn192(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
 int clusters_cg1(int bn, int cluster);     // max_active_clusters of the single-CTA kernels (ge_inst_cg1_*.cu)
 int clusters_cg1_bn64(int cluster);
 int clusters_cg1_bn128(int cluster);
 int clusters_cg1_bn192(int cluster);
 int clusters_cg1_bn256(int cluster);
-cudaError_t launch_cg1_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn128(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn256(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn512(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn512_mc(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn256_mc(bool, bool, bool, bool, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn256(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn128(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn512(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn512_mc(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256_mc(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
 int clusters_mc(int bn);     // co-resident 4-CTA multicast clusters of the (bn, pair) kernel
 
 }  // namespace ge

@@ -155,8 +155,13 @@ def test_plan_tiles(ge):
     assert p["tile_m"] == 128 and p["tile_n"] == 256 and p["num_tiles"] == 64 * 32
     p = ge.plan(8192, 8192, 8192, tile_n=256, cta_group=2)
     assert p["tile_m"] == 256 and p["num_tiles"] == 32 * 32
-    p = ge.plan(35, 8457, 2560)                        # skinny M: 128 x 128 tiles (measured best, HBM bound)
-    assert (p["tile_n"], p["cta_group"]) == (128, 1) and p["num_tiles"] == 67 and p["stream_k_tiles"] == 0
+    p = ge.plan(35, 8457, 2560)                        # skinny M: swap-AB, N = 8457 on the 128-row MMA side
+    assert p["swap_ab"] == 1 and (p["tile_n"], p["cta_group"]) == (64, 1) and p["num_tiles"] == 67
+    p = ge.plan(35, 8457, 2560, swap_ab=1)             # unswapped: 128 x 128 tiles over the 8457 columns
+    assert p["swap_ab"] == 0 and (p["tile_n"], p["cta_group"]) == (128, 1) and p["num_tiles"] == 67
+    assert ge.plan(35, 8457, 2560, prologue="scale_k")["swap_ab"] == 0           # prologue on A: no swap
+    assert ge.plan(35, 8457, 2560, bias_mode="full")["swap_ab"] == 0             # FULL bias: no swap
+    assert ge.plan(300, 520, 200, swap_ab=2)["swap_ab"] == 1                     # forced where legal
     p = ge.plan(1024, 1024, 1024)                      # small: narrow tiles to fill the SMs
     assert p["tile_n"] == 64 and p["num_tiles"] == 128
     p = ge.plan(2048, 2048, 2048, batch=64)           # large: the 256 x 256 CTA-pair tile

@@ -51,7 +51,8 @@ def run_gpu(prob, layouts="rr", *, op=None, out_dtype=torch.float16, lda=None, l
     scale = prob.scale.cuda() if prob.scale is not None else None
     if prob.meta.get("prologue") == "hadamard":
         scale = dev_tile(prob.scale, layouts[0])
-    C = ge.gemm_epilogue(A, B, bias, op=op, bias_mode=prob.meta.get("bias_mode") or "row",
+    bm = prob.meta.get("bias_mode")
+    C = ge.gemm_epilogue(A, B, bias, op=op, bias_mode=bm if bm in ("row", "col", "full") else "row",
                          prologue=prob.meta.get("prologue"), scale=scale, out_dtype=out_dtype, **kw)
     torch.cuda.synchronize()
     return C.float().cpu().numpy().astype(np.float64)
@@ -102,6 +103,8 @@ def test_golden_cases_on_gpu(case, layouts):
     B = torch.tensor(case["B"], dtype=torch.float16).reshape(K, N)
     bias = None if case["bias"] is None else torch.tensor(case["bias"], dtype=torch.float16)
     scale = None if case.get("scale") is None else torch.tensor(case["scale"], dtype=torch.float32)
+    if case["prologue"] == "hadamard":
+        scale = torch.tensor(case["S"], dtype=torch.float16).reshape(M, K)
     prob = workloads.Problem(M, N, K, A, B, bias, scale, {"bias_mode": case["bias_mode"], "prologue": case["prologue"]})
     op = ("bias_" if bias is not None else "") + ("relu" if case["relu"] else "")
     op = {"bias_": "bias", "": "none"}.get(op, op)
@@ -719,3 +722,49 @@ def test_hadamard_batched_and_host():
     Cd = ge.gemm_epilogue(A[0], B[0], bias, prologue="hadamard", scale=S[0])
     torch.cuda.synchronize()
     assert torch.equal(Ch, Cd.cpu())
+
+
+# ------------------------------------------------------------------ swap-AB (skinny M)
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+@pytest.mark.parametrize("bias_mode,op,out_dtype", [("row", "bias_relu", torch.float16), ("col", "bias_relu", torch.float32),
+                                                   ("row", "sub_bias_sigmoid", torch.float16), (None, "relu", torch.float16),
+                                                   ("row", "literal_bias_relu", torch.float16)])
+def test_swap_ab_exact_and_bound(layouts, bias_mode, op, out_dtype):
+    """C^T = B^T A^T with a transposed store: forced on a ragged problem (M = 37 rows of C become the
+    MMA's N, N = 1000 its 128-row side) and on a tile-exact one; ROW and COL bias trade places.
+    Small integers bitwise, uniform data within the bound (sigmoid: bound only)."""
+    for M, N, K in ((37, 1000, 200), (64, 256, 128)):
+        for kind in ("smallint", "uniform"):
+            prob = workloads.make_problem(M, N, K, seed=120, kind=kind, bias_mode=bias_mode or "none")
+            assert ge.plan(M, N, K, layouts=layouts, swap_ab=2, bias_mode=bias_mode or "row")["swap_ab"] == 1
+            got = run_gpu(prob, layouts, op=op, out_dtype=out_dtype, swap_ab=2)
+            act = "sigmoid" if "sigmoid" in op else "relu"
+            out, mag = oracle_run(prob, layouts, act=act, bias_sub=op.startswith("sub"),
+                                  literal_round=op.startswith("literal"))
+            if kind == "smallint" and act == "relu":
+                assert np.array_equal(got, exact_expect(out, out_dtype)), (M, N, K, layouts)
+            else:
+                check_bound(got, out, mag, f"swap {M}x{N}x{K} {layouts}")
+
+
+def test_swap_ab_batched_padding_and_default():
+    """Batched swap-AB (per-item bias), C padding untouched, and the default plan of a skinny
+    shape takes the swapped path (BASELINE configs[2] b, scaled down)."""
+    assert ge.plan(35, 8457, 2560)["swap_ab"] == 1
+    batch, M, N, K = 3, 35, 1030, 136
+    probs = [workloads.make_problem(M, N, K, seed=130 + b, kind="smallint", bias_mode="row") for b in range(batch)]
+    A = torch.stack([p.A for p in probs]).cuda()
+    Bpad = torch.zeros((batch, K, 1032), dtype=torch.float16)        # ldb padded to 16 B (TMA)
+    Bpad[:, :, :N] = torch.stack([p.B for p in probs])
+    B = Bpad.cuda()[:, :, :N]
+    bias = torch.stack([p.bias for p in probs]).cuda()
+    Cbuf = torch.full((batch, M, 1040), -5.0, dtype=torch.float16, device="cuda")
+    ge.gemm_epilogue_batched(A, B, bias, out=Cbuf[:, :, :N], swap_ab=2)
+    torch.cuda.synchronize()
+    assert (Cbuf[:, :, N:] == -5.0).all()
+    for b, p in enumerate(probs):
+        out, _ = oracle_run(p, "rr")
+        assert np.array_equal(Cbuf[b, :, :N].float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+    unswapped = ge.gemm_epilogue_batched(A, B, bias, swap_ab=1)
+    torch.cuda.synchronize()
+    assert torch.equal(unswapped, Cbuf[:, :, :N])          # exact data: both orders agree bitwise
