@@ -974,8 +974,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             ptx::st_async_v4(dst + g * 512, v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3], rbar);
                     }
                     const long long tr0 = clock64();
+                    if (dbg && lane == 0) dl[DBG_EPI_TMEMLD] += static_cast<unsigned long long>(tr0 - tw0);  // sends
                     ptx::mbar_wait(recv_full_bar, 0);
                     if (dbg && e_idx == 0 && lane == 0) dl[DBG_SK_WRITE] += static_cast<unsigned long long>(clock64() - tr0);
+                    const long long to0 = clock64();
 #pragma unroll 1
                     for (int j = 0; j < CPH; ++j) {
                         const int c = j * NG + grp;
@@ -999,6 +1001,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         compute(c, v, w);
                         store(c, w);
                     }
+                    if (dbg && lane == 0) dl[DBG_EPI_MATH] += static_cast<unsigned long long>(clock64() - to0);   // owner
                     release(0);
                     if (dbg && e_idx == 0 && lane == 0) dl[DBG_EPI_TILE] += static_cast<unsigned long long>(clock64() - t_epi0);
                     continue;
