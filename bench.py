@@ -568,7 +568,8 @@ def compare_torch(torch, w, stream, iters=10):
     torch unfused matmul + add + relu (cuBLAS + 2 elementwise kernels, the paper's baseline shape,
     PAPER.md:1255-1260), torch._addmm_activation (cuBLASLt bias+ReLU epilogue) and plain
     torch.matmul.  Each runs as one CUDA graph of the same number of calls as our timed region, over
-    the same rotating operand sets (first layout of each set).
+    the same rotating operand sets and the same layouts in the same order (cuBLAS picks its kernel
+    per layout, so both sides switch kernels alike).
     Like-for-like alignment: when N is not a multiple of 8, the library computes the padded
     N' = ld8(N) columns of the same padded operand storage we read, so its C rows are 16-byte
     aligned like ours (TFLOP/s still counts the logical 2MNK)."""
@@ -576,20 +577,20 @@ def compare_torch(torch, w, stream, iters=10):
     M, N, K = w.M, w.N, w.K
     fl = 2.0 * M * N * K
     Np = w.ld8(N)
-    lay0 = w.sets[0][0][0]
-    pad = Np != N and lay0[1] == "r"
+    layouts = [lay for lay, _, _ in w.sets[0]]
+    pad = Np != N
     bias = w.bias if not pad else torch.cat([w.bias, torch.zeros(Np - N, dtype=w.bias.dtype, device=w.bias.device)])
 
-    def operands(cur):
-        lay, A, B = cur[0]
+    def operands(lay, A, B):
         a, b = A[0], B[0]
-        if pad:
+        if pad and lay[1] == "r":
             b = torch.as_strided(b, (K, Np), (b.stride(0), 1))     # the padded storage row pitch (ld8(N))
-        return a, b
+        return a, b                  # col-major B keeps N columns (its C rows then have ldc = N)
 
     def t(fn, it=iters):
         """One CUDA graph of `it` calls rotating the operand sets, replayed once (our protocol)."""
-        ops = [operands(cur) for cur in w.sets]
+        # every layout of every operand set, in the order of our steps (the same kernel mix)
+        ops = [operands(lay, A, B) for cur in w.sets for lay, A, B in cur]
         for a, b in ops[:2]:
             fn(a, b)
         torch.cuda.synchronize()
@@ -606,10 +607,11 @@ def compare_torch(torch, w, stream, iters=10):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / it * 1e-3
     try:
-        out["torch_unfused_matmul_add_relu"] = fl / t(lambda a, b: torch.relu_(torch.matmul(a, b).add_(bias))) / 1e12
+        bias_for = lambda b: bias if b.shape[1] == bias.shape[0] else w.bias
+        out["torch_unfused_matmul_add_relu"] = fl / t(lambda a, b: torch.relu_(torch.matmul(a, b).add_(bias_for(b)))) / 1e12
         out["torch_matmul_only"] = fl / t(lambda a, b: torch.matmul(a, b)) / 1e12
-        out["cublaslt_addmm_relu"] = fl / t(lambda a, b: torch._addmm_activation(bias, a, b)) / 1e12
-        out["layout"] = lay0
+        out["cublaslt_addmm_relu"] = fl / t(lambda a, b: torch._addmm_activation(bias_for(b), a, b)) / 1e12
+        out["layouts"] = layouts
         out["ldc"] = Np if pad else N
         out["protocol"] = (f"one CUDA graph of {iters} calls over the same rotating operand sets, replayed once "
                            "(as our timed region)" + ("; N padded to ld8(N) for 16-B aligned C rows" if pad else ""))

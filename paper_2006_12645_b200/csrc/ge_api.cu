@@ -470,6 +470,7 @@ int group_m_for(const Plan& pl, const Args& a, int sms) {
 unsigned long long* g_dbg[64] = {};
 int g_dbg_ctas[64] = {};
 int g_dbg_last = -1;                    // device of the last launch (read by ge_debug_read)
+#if GE_DBG
 unsigned long long* debug_buffer(int sms) {
     static const bool on = getenv("GE_DEBUG_STATS") != nullptr;
     if (!on) return nullptr;
@@ -488,6 +489,7 @@ unsigned long long* debug_buffer(int sms) {
     g_dbg_last = dev;
     return g_dbg[dev];
 }
+#endif
 
 // ------------------------------------------------------------------ tensor maps
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -701,6 +703,8 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
     p.batch = static_cast<int>(a.batch);
     p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg * (pl.mc ? 2 : 1)));
     p.num_n_tiles = static_cast<int>(cdiv(a.N, pl.bn));
+    p.a_mn = a_mn ? 1 : 0;
+    p.b_mn = b_mn ? 1 : 0;
     p.num_k_blocks1 = static_cast<int>(cdiv(a.K, ge::kBK));
     p.num_k_blocks = p.num_k_blocks1 + static_cast<int>(cdiv(a.K2, ge::kBK));
     p.group_m = group_m_for(pl, a, sms);
@@ -764,18 +768,18 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
     const int grid = static_cast<int>(std::max<int64_t>(plan.clusters, 1) * plan.cg * (plan.mc ? 2 : 1));
     cudaError_t e;
     if (pl.mc) {
-        if (pl.bn == 512) e = ge::launch_cg2_bn512_mc(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else e = ge::launch_cg2_bn256_mc(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        if (pl.bn == 512) e = ge::launch_cg2_bn512_mc(f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg2_bn256_mc(f32, pro, maps, p, grid, st);
     } else if (pl.cg == 1) {
-        if (pl.bn == 64) e = ge::launch_cg1_bn64(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else if (pl.bn == 128) e = ge::launch_cg1_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else if (pl.bn == 192) e = ge::launch_cg1_bn192(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else e = ge::launch_cg1_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        if (pl.bn == 64) e = ge::launch_cg1_bn64(f32, pro, maps, p, grid, st);
+        else if (pl.bn == 128) e = ge::launch_cg1_bn128(f32, pro, maps, p, grid, st);
+        else if (pl.bn == 192) e = ge::launch_cg1_bn192(f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg1_bn256(f32, pro, maps, p, grid, st);
     } else {
-        if (pl.bn == 128) e = ge::launch_cg2_bn128(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else if (pl.bn == 192) e = ge::launch_cg2_bn192(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else if (pl.bn == 256) e = ge::launch_cg2_bn256(a_mn, b_mn, f32, pro, maps, p, grid, st);
-        else e = ge::launch_cg2_bn512(a_mn, b_mn, f32, pro, maps, p, grid, st);
+        if (pl.bn == 128) e = ge::launch_cg2_bn128(f32, pro, maps, p, grid, st);
+        else if (pl.bn == 192) e = ge::launch_cg2_bn192(f32, pro, maps, p, grid, st);
+        else if (pl.bn == 256) e = ge::launch_cg2_bn256(f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg2_bn512(f32, pro, maps, p, grid, st);
     }
     if (e != cudaSuccess) {
         cudaGetLastError();

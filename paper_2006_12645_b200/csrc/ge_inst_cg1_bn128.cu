@@ -1,10 +1,10 @@
-// Instantiates the fused kernel family for BN = 128, cta_group = 1 (24 layout/dtype/prologue variants).
+// Instantiates the fused kernel family for BN = 128, cta_group = 1 (6 dtype/prologue variants; layouts are runtime).
 #include "ge_launch.cuh"
 
 namespace ge {
-cudaError_t launch_cg1_bn128(bool a_mn, bool b_mn, bool f32, int pro, const Maps& m, const Params& p, int grid,
+cudaError_t launch_cg1_bn128(bool f32, int pro, const Maps& m, const Params& p, int grid,
                             cudaStream_t st) {
-    return launch_bn_cg<128, 1>(a_mn, b_mn, f32, pro, m, p, grid, st);
+    return launch_bn_cg<128, 1>(f32, pro, m, p, grid, st);
 }
 int clusters_cg1_bn128(int cluster) { return max_active_clusters<128, 1>(cluster); }
 }  // namespace ge

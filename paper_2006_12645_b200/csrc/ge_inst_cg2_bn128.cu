@@ -1,9 +1,9 @@
-// Instantiates the fused kernel family for BN = 128, cta_group = 2 (24 layout/dtype/prologue variants).
+// Instantiates the fused kernel family for BN = 128, cta_group = 2 (6 dtype/prologue variants; layouts are runtime).
 #include "ge_launch.cuh"
 
 namespace ge {
-cudaError_t launch_cg2_bn128(bool a_mn, bool b_mn, bool f32, int pro, const Maps& m, const Params& p, int grid,
+cudaError_t launch_cg2_bn128(bool f32, int pro, const Maps& m, const Params& p, int grid,
                             cudaStream_t st) {
-    return launch_bn_cg<128, 2>(a_mn, b_mn, f32, pro, m, p, grid, st);
+    return launch_bn_cg<128, 2>(f32, pro, m, p, grid, st);
 }
 }  // namespace ge

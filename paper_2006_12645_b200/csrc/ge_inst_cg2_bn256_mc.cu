@@ -3,8 +3,8 @@
 #include "ge_launch.cuh"
 
 namespace ge {
-cudaError_t launch_cg2_bn256_mc(bool a_mn, bool b_mn, bool f32, int pro, const Maps& m, const Params& p, int grid,
+cudaError_t launch_cg2_bn256_mc(bool f32, int pro, const Maps& m, const Params& p, int grid,
                                cudaStream_t st) {
-    return launch_bn_cg<256, 2, true>(a_mn, b_mn, f32, pro, m, p, grid, st);
+    return launch_bn_cg<256, 2, true>(f32, pro, m, p, grid, st);
 }
 }  // namespace ge

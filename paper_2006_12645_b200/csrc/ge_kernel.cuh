@@ -79,7 +79,10 @@ constexpr int kBK = 64;                 // K per pipeline stage (64 fp16 = one 1
 constexpr int kUmmaK = 16;              // K per tcgen05.mma for 16-bit inputs
 constexpr int kRowsPerCta = 128;        // accumulator rows per CTA (= TMEM lanes)
 constexpr int kSmemBudget = 232448;     // 227 KB dynamic smem per CTA on sm_100
-constexpr int kXformWarps = 4;     // prologue transform warps (PRO kernels)
+#ifndef GE_XFORM_WARPS
+#define GE_XFORM_WARPS 4
+#endif
+constexpr int kXformWarps = GE_XFORM_WARPS;    // prologue transform warps (PRO kernels)
 constexpr int kStagingSetBytes = 16384; // one staging buffer per epilogue warp: 8 x 2 KB (fp16) or 4 x 4 KB (fp32)
 
 enum : int { BIAS_NONE = -1, BIAS_ROW = 0, BIAS_COL = 1, BIAS_FULL = 2 };
@@ -90,6 +93,7 @@ struct Params {
     int M, N, K, batch;
     int num_m_tiles, num_n_tiles, num_k_blocks;
     int num_k_blocks1;              // k-blocks of A.B; the rest come from P.Q (sum of matmuls, Listing 4)
+    int a_mn, b_mn;                 // operand majorness: A column-major (MN-major), B row-major (MN-major)
     int group_m;                    // raster group (m-tiles per group) for L2 locality
     long long num_tiles;
     // epilogue
@@ -140,7 +144,9 @@ enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY
              DBG_MMA_END = 14, DBG_FIRST_MMA = 15,
              // %globaltimer (ns) of: kernel entry, end of setup (barriers, TMEM, cluster sync), the end
              // of this CTA's epilogue, and its exit (after teardown)
-             DBG_G_ENTRY = 16, DBG_G_START = 17, DBG_G_EPI_END = 18, DBG_G_EXIT = 19, DBG_SLOTS = 20 };
+             DBG_G_ENTRY = 16, DBG_G_START = 17, DBG_G_EPI_END = 18, DBG_G_EXIT = 19,
+             // prologue transform warps: cycles blocked on a landed stage, cycles rewriting stages
+             DBG_XF_WAIT = 20, DBG_XF_WORK = 21, DBG_SLOTS = 22 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -311,7 +317,9 @@ __host__ __device__ constexpr int kernel_threads(bool out_f32, bool pro) {
 // operand traffic per flop); data-parallel tiles only (no prologue, stream-K or split-K).
 // PRO: 0 no prologue; 1 in-place prologue op on the A stage (SCALE_K / RELU); 2 the same with the
 // Hadamard tile S staged by TMA next to A (its second input dataspace).
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, int PRO, int CG, bool MC = false>
+// The operand layouts (K- or MN-major A and B) are runtime parameters (Params::a_mn / b_mn): one
+// instantiation serves the four layout pairs, so a step that alternates layouts runs one kernel.
+template <int BN, bool OUT_F32, int PRO, int CG, bool MC = false>
 __global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO != 0), 1)
 ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_p,
@@ -325,7 +333,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     constexpr int NH = C_::kNHalves;
     constexpr int HALF_COLS = BN / NH;
     constexpr bool kPairAcq = GE_PAIR_ACQ && !PRO && NH == 1 && !MC && GE_PAIR_RELEASE;
-    constexpr uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, C_::kUmmaN, A_MN, B_MN);
+    const bool A_MN = p.a_mn != 0, B_MN = p.b_mn != 0;       // MN-major (row-major B / col-major A)
+    const uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, C_::kUmmaN, A_MN, B_MN);
 
     const unsigned long long g_entry = GE_DBG ? globaltimer() : 0ull;
     extern __shared__ uint8_t smem_raw[];
@@ -466,7 +475,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     };
                     // A, and the Hadamard tile S with A's box and swizzle (element-aligned with A in smem)
                     auto load_a = [&](uint8_t* dst, const CUtensorMap* map, int cb) {
-                        if constexpr (A_MN) {
+                        if (A_MN) {
 #pragma unroll
                             for (int i = 0; i < kRowsPerCta / 64; ++i) load(dst + i * 8192, map, m0 + i * 64, k0, pol_a, cb);
                         } else {
@@ -483,13 +492,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             // this CTA's 64-row half `pair` of the block, to both pairs' CTAs of rank `rank`
                             // (an MN-major half is one 64-wide swizzle atom; the K-major map's box is 64 rows)
                             const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
-                            if constexpr (B_MN)
+                            if (B_MN)
                                 ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], nh + pair * 64, k0, b,
                                                          mask, pol_b);
                             else
                                 ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], k0, nh + pair * 64, b,
                                                          mask, pol_b);
-                        } else if constexpr (B_MN) {
+                        } else if (B_MN) {
 #pragma unroll
                             for (int i = 0; i < C_::kBBlockRows / 64; ++i)
                                 load(sbh + i * 8192, map_b, nh + i * 64, k0, pol_b, b);
@@ -533,8 +542,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 // plus the stage offset (the 14-bit address field cannot carry: smem < 256 KB).
                 const uint64_t a_desc0 = ptx::make_sw128_desc(a_base, A_MN ? 8192 : 0, 1024);
                 const uint64_t b_desc0 = ptx::make_sw128_desc(b_base, B_MN ? 8192 : 0, 1024);
-                constexpr int A_STEP = A_MN ? 2048 / 16 : 32 / 16;
-                constexpr int B_STEP = B_MN ? 2048 / 16 : 32 / 16;
+                const uint64_t A_STEP = A_MN ? 2048 / 16 : 32 / 16;
+                const uint64_t B_STEP = B_MN ? 2048 / 16 : 32 / 16;
                 auto desc_a = [&](int stage) {
                     return a_desc0 + static_cast<uint64_t>((stage * C_::kAStage) >> 4);
                 };
@@ -546,8 +555,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     if (!GE_PAIR_RELEASE || (stage & 1)) ptx::mma_commit_elect<CG>(&empty_bar[stage], MC ? 0xF : 0x3);
                 };
                 auto mma_half = [&](int stage, int kb, int h) {
-                    ptx::mma_kblock<CG, A_STEP, B_STEP>(d_tmem + h * C_::kUmmaN, desc_a(stage), desc_b(stage, h), IDESC,
-                                                        kb != pc.kb0);
+                    ptx::mma_kblock<CG>(d_tmem + h * C_::kUmmaN, desc_a(stage), desc_b(stage, h), IDESC, kb != pc.kb0,
+                                        A_STEP, B_STEP);
                 };
                 if constexpr (NH == 2) {
                     // Single 512-column accumulator, drained half by half by the epilogue.  Half-0
@@ -582,8 +591,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             s_pend = s;
                         }
                         if (h1_free) {
-                            ptx::mma_kblock2<CG, A_STEP, B_STEP>(d_tmem, desc_a(s), desc_b(s, 0), desc_b(s, 1), IDESC,
-                                                                 kb != pc.kb0);
+                            ptx::mma_kblock2<CG>(d_tmem, desc_a(s), desc_b(s, 0), desc_b(s, 1), IDESC, kb != pc.kb0,
+                                                 A_STEP, B_STEP);
                             release_stage(s);
                         } else {
                             mma_half(s, kb, 0);
@@ -668,8 +677,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         constexpr int NBUF = C_::kStagingBufs;
         uint8_t* stage_c = smem_c + e_idx * (NBUF * STG);
         const uint64_t pol_c = ptx::l2_policy(p.hint_c);
+        // ROW bias (staged in smem) or COL bias (one value per thread: swap-AB turns the ROW bias of
+        // C into a COL bias of C^T), ReLU, single rounding
         const bool epi_fast = (C_::kBiasF32 || (GE_EPI_FAST512 && p.bias_sign > 0.0f)) && !p.literal && p.act == ACT_RELU &&
-                              p.bias_mode == BIAS_ROW && !(GE_DBG && p.dbg_flags);
+                              (p.bias_mode == BIAS_ROW || p.bias_mode == BIAS_COL) && !(GE_DBG && p.dbg_flags);
         int buf = 0;
         for (int jj = 0; jj < work.count(); ++jj) {
             const int it = work.epi_index(jj);
@@ -743,7 +754,11 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // with the general code inline, so it also gets its own chunk loop below.
             auto compute_fast = [&](const int c, const uint32_t* v, uint32_t* w) {
                 uint32_t r[W];
-                if constexpr (C_::kBiasF32) {
+                if (p.bias_mode == BIAS_COL) {
+                    const float bc = p.bias_sign * beta_col;
+#pragma unroll
+                    for (int e = 0; e < W / 2; ++e) ptx::add_f32x2(v[2 * e], v[2 * e + 1], bc, bc, r[2 * e], r[2 * e + 1]);
+                } else if constexpr (C_::kBiasF32) {
                     const float4* bs = reinterpret_cast<const float4*>(smem_bias_f + c * W);  // broadcast reads
 #pragma unroll
                     for (int g = 0; g < W / 4; ++g) {
@@ -1173,21 +1188,23 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         // "Prologue"): loading A through registers (ld.global -> op -> st.shared, the paper's Volta copy
         // path) saves two smem passes but its global loads could not be kept in flight deep enough
         // (2-4x slower at 4096^3), so the TMA stays the loader.
-        const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0..127
-        // Thread xt rewrites the 16-B chunks o = (i*128 + xt)*16, i = 0..7, of each 16 KB A stage.
-        //  K-major stage (row = m, 128-B rows of 64 k, 128-B swizzle): the logical k-chunk of all
-        //   eight chunks is kc = (xt % 8) ^ ((xt / 8) % 8), so the thread needs scale[k0+8kc .. +8];
-        //  MN-major stage (row = k, 64-m atoms of 8 KB): chunk i lies on k = k0 + (16i + xt/8) % 64.
+        constexpr int XT = kXformWarps * 32;                     // transform threads
+        const int xt = threadIdx.x - (4 + EPI_WARPS) * 32;      // 0 .. XT-1
+        // Thread xt rewrites the 16-B chunks o = (i*XT + xt)*16, i < 16 KB / 16 / XT, of each A stage.
+        //  K-major stage (row = m, 128-B rows of 64 k, 128-B swizzle): the logical k-chunk of all its
+        //   chunks is kc = (xt % 8) ^ ((xt / 8) % 8) (XT is a multiple of 64), so the thread needs
+        //   scale[k0+8kc .. +8];
+        //  MN-major stage (row = k, 64-m atoms of 8 KB): chunk i lies on k = k0 + ((i*XT + xt)/8) % 64.
         // The 8 scale values of the NEXT k-block are prefetched while the current one is
         // transformed (the scale vector would otherwise cost an L2 round trip per chunk).
         const bool scale_k = p.prologue == PRO_SCALE_K;
         const int kc = (xt & 7) ^ ((xt >> 3) & 7);
         auto fetch = [&](int kb, float* dst) {
             const int k0 = kb * kBK;
-            if constexpr (A_MN) {
+            if (A_MN) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = k0 + ((i * 16 + (xt >> 3)) & 63);
+                for (int i = 0; i < C_::kAStage / 16 / XT; ++i) {
+                    const int k = k0 + (((i * XT + xt) >> 3) & 63);
                     dst[i] = k < p.K ? __ldg(p.scale + k) : 0.0f;
                 }
             } else {
@@ -1217,12 +1234,14 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     if (kn == pc.kb1) kn = (wi + 1 < work.count()) ? work.get(wi + 1).kb0 : 0;
                     fetch(kn, sc_nxt);                                // in flight during this stage
                 }
+                const long long tx0 = dbg ? clock64() : 0;
                 ptx::mbar_wait(&full_bar[s], phase);
+                const long long tx1 = dbg ? clock64() : 0;
                 uint8_t* sa = smem_a + s * C_::kAStage;
-                constexpr int NCH = C_::kAStage / 16 / 128;          // 8 chunks per thread
+                constexpr int NCH = C_::kAStage / 16 / XT;           // chunks per thread
                 uint4 x[NCH];
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) x[i] = *reinterpret_cast<const uint4*>(sa + (i * 128 + xt) * 16);
+                for (int i = 0; i < NCH; ++i) x[i] = *reinterpret_cast<const uint4*>(sa + (i * XT + xt) * 16);
                 if constexpr (PRO == 2) {
                     // HADAMARD: a' = RNE_fp16(s(i,k) * a(i,k)); S sits at the same swizzled offsets as A
                     // (same box, same swizzle), and the fp16 x fp16 product is exact before its one
@@ -1230,7 +1249,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     const uint8_t* ss = smem_s + s * C_::kSStage;
 #pragma unroll
                     for (int i = 0; i < NCH; ++i) {
-                        const uint4 y = *reinterpret_cast<const uint4*>(ss + (i * 128 + xt) * 16);
+                        const uint4 y = *reinterpret_cast<const uint4*>(ss + (i * XT + xt) * 16);
                         __half2* h2 = reinterpret_cast<__half2*>(&x[i]);
                         const __half2* s2 = reinterpret_cast<const __half2*>(&y);
 #pragma unroll
@@ -1262,12 +1281,16 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < NCH; ++i) *reinterpret_cast<uint4*>(sa + (i * 128 + xt) * 16) = x[i];
+                for (int i = 0; i < NCH; ++i) *reinterpret_cast<uint4*>(sa + (i * XT + xt) * 16) = x[i];
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
                     if (CG == 2 && !leader) ptx::mbar_arrive_cluster(&xform_bar[s], 0);
                     else ptx::mbar_arrive(&xform_bar[s]);
+                }
+                if (dbg && lane == 0) {
+                    dl[DBG_XF_WAIT] += static_cast<unsigned long long>(tx1 - tx0);
+                    dl[DBG_XF_WORK] += static_cast<unsigned long long>(clock64() - tx1);
                 }
                 if (++s == S) { s = 0; phase ^= 1; }
             }

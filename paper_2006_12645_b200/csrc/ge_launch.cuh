@@ -19,9 +19,9 @@ struct Maps {
 int smem_bytes_for(int bn, int cg, bool sx = false);
 int stages_for(int bn, int cg, bool sx = false);
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, int PRO, int CG, bool MC = false>
+template <int BN, bool OUT_F32, int PRO, int CG, bool MC = false>
 cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st) {
-    auto kern = ge_fused_kernel<BN, A_MN, B_MN, OUT_F32, PRO, CG, MC>;
+    auto kern = ge_fused_kernel<BN, OUT_F32, PRO, CG, MC>;
     constexpr int smem = Cfg<BN, CG, PRO == 2>::kSmemBytes;
     static bool attr_done = false;   // benign race: setting the attribute twice is harmless
     if (!attr_done) {
@@ -58,7 +58,7 @@ cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st
 // query fails); the split-K planner uses it (cluster scheduling is GPC-bound, not SM-count-bound).
 template <int BN, int CG, bool MC = false>
 int max_active_clusters(int cluster) {
-    auto kern = ge_fused_kernel<BN, false, false, false, 0, CG, MC>;
+    auto kern = ge_fused_kernel<BN, false, 0, CG, MC>;
     constexpr int smem = Cfg<BN, CG>::kSmemBytes;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
         cudaGetLastError();
@@ -83,49 +83,43 @@ int max_active_clusters(int cluster) {
     return n;
 }
 
-// Dispatch over the 24 (A_MN, B_MN, OUT_F32, PRO in {0, 1, 2}) variants of one (BN, CG) configuration.
+// Dispatch over the 6 (OUT_F32, PRO in {0, 1, 2}) variants of one (BN, CG) configuration; the operand
+// layouts travel in Params (a_mn / b_mn), and the host rejects the one unsupported layout (BN = 192
+// CTA pairs stage 96 B rows per CTA: K-major B only, ge_api.cu validate()).
 template <int BN, int CG, bool MC = false>
-cudaError_t launch_bn_cg(bool a_mn, bool b_mn, bool f32, int pro, const Maps& m, const Params& p, int grid,
-                         cudaStream_t st) {
-    const int key = (a_mn ? 4 : 0) | (b_mn ? 2 : 0) | (f32 ? 1 : 0);
-    switch (key * 3 + pro) {
-// (BN = 192 with CTA pairs stages 96 B rows per CTA: only K-major B, whose TMA box takes any row
-// count; an MN-major B stage is built from 64-column swizzle atoms.)
-#define GE_CASE(K, AM, BM, F, P)                                                  \
-    case K * 3 + P:                                                               \
-        if constexpr ((BM && BN == 192 && CG == 2) || (MC && P)) return cudaErrorInvalidValue; \
-        else return launch_one<BN, AM, BM, F, P, CG, MC>(m, p, grid, st);
-#define GE_CASES(K, AM, BM, F) GE_CASE(K, AM, BM, F, 0) GE_CASE(K, AM, BM, F, 1) GE_CASE(K, AM, BM, F, 2)
-        GE_CASES(0, false, false, false)
-        GE_CASES(1, false, false, true)
-        GE_CASES(2, false, true, false)
-        GE_CASES(3, false, true, true)
-        GE_CASES(4, true, false, false)
-        GE_CASES(5, true, false, true)
-        GE_CASES(6, true, true, false)
-        GE_CASES(7, true, true, true)
-#undef GE_CASES
+cudaError_t launch_bn_cg(bool f32, int pro, const Maps& m, const Params& p, int grid, cudaStream_t st) {
+    switch ((f32 ? 3 : 0) + pro) {
+#define GE_CASE(F, P)                                                             \
+    case (F ? 3 : 0) + P:                                                         \
+        if constexpr (MC && P) return cudaErrorInvalidValue;                      \
+        else return launch_one<BN, F, P, CG, MC>(m, p, grid, st);
+        GE_CASE(false, 0)
+        GE_CASE(false, 1)
+        GE_CASE(false, 2)
+        GE_CASE(true, 0)
+        GE_CASE(true, 1)
+        GE_CASE(true, 2)
 #undef GE_CASE
     }
     return cudaErrorInvalidValue;
 }
 
 // Defined in ge_inst_*.cu (one translation unit per configuration, compiled in parallel).
-cudaError_t launch_cg1_bn64(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg1_bn128(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg1_bn192(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn192(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn64(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn128(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn192(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn192(bool, int, const Maps&, const Params&, int, cudaStream_t);
 int clusters_cg1(int bn, int cluster);     // max_active_clusters of the single-CTA kernels (ge_inst_cg1_*.cu)
 int clusters_cg1_bn64(int cluster);
 int clusters_cg1_bn128(int cluster);
 int clusters_cg1_bn192(int cluster);
 int clusters_cg1_bn256(int cluster);
-cudaError_t launch_cg1_bn256(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn128(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn256(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn512(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn512_mc(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
-cudaError_t launch_cg2_bn256_mc(bool, bool, bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg1_bn256(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn128(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn512(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn512_mc(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256_mc(bool, int, const Maps&, const Params&, int, cudaStream_t);
 int clusters_mc(int bn);     // co-resident 4-CTA multicast clusters of the (bn, pair) kernel
 
 }  // namespace ge

@@ -352,15 +352,17 @@ __device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a_desc, 
     "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a2, b2, %3, t;\n\t"                           \
     "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a3, b3, %3, t;\n\t}"
 
-template <int CG, int A_STEP, int B_STEP>
+// a_step / b_step: the K = 16 step of each operand in 16-B descriptor units (2 for K-major, 128 for
+// MN-major: the operand layouts are runtime values, one kernel serves all four layout pairs).
+template <int CG>
 __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
-                                           uint32_t accumulate) {
+                                           uint32_t accumulate, uint64_t a_step, uint64_t b_step) {
     if constexpr (CG == 1) {
         asm volatile(GE_MMA_KBLOCK_ASM("1")
-                     ::"r"(d_tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+                     ::"r"(d_tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "l"(a_step), "l"(b_step));
     } else {
         asm volatile(GE_MMA_KBLOCK_ASM("2")
-                     ::"r"(d_tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+                     ::"r"(d_tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate), "l"(a_step), "l"(b_step));
     }
 }
 
@@ -381,15 +383,15 @@ __device__ __forceinline__ void mma_kblock(uint32_t d_tmem, uint64_t ad, uint64_
     "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], a3, b3, %4, t;\n\t"                           \
     "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [d1], a3, c3, %4, t;\n\t}"
 
-template <int CG, int A_STEP, int B_STEP>
+template <int CG>
 __device__ __forceinline__ void mma_kblock2(uint32_t d_tmem, uint64_t ad, uint64_t bd0, uint64_t bd1, uint32_t idesc,
-                                            uint32_t accumulate) {
+                                            uint32_t accumulate, uint64_t a_step, uint64_t b_step) {
     if constexpr (CG == 1) {
         asm volatile(GE_MMA_KBLOCK2_ASM("1")
-                     ::"r"(d_tmem), "l"(ad), "l"(bd0), "l"(bd1), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+                     ::"r"(d_tmem), "l"(ad), "l"(bd0), "l"(bd1), "r"(idesc), "r"(accumulate), "l"(a_step), "l"(b_step));
     } else {
         asm volatile(GE_MMA_KBLOCK2_ASM("2")
-                     ::"r"(d_tmem), "l"(ad), "l"(bd0), "l"(bd1), "r"(idesc), "r"(accumulate), "n"(A_STEP), "n"(B_STEP));
+                     ::"r"(d_tmem), "l"(ad), "l"(bd0), "l"(bd1), "r"(idesc), "r"(accumulate), "l"(a_step), "l"(b_step));
     }
 }
 

@@ -7,6 +7,7 @@ import paper_2006_12645_b200 as ge
 M, N, K = (int(x) for x in sys.argv[1:4]); lay = sys.argv[4]; bn, cg = int(sys.argv[5]), int(sys.argv[6])
 sk = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 mc = int(sys.argv[8]) if len(sys.argv) > 8 else 0
+pro = sys.argv[9] if len(sys.argv) > 9 else None
 ld8 = lambda n: (n + 7) // 8 * 8          # padded leading dimensions (16-byte TMA pitch), like bench.py
 def operand(rows, cols, l):
     if l == "r":
@@ -15,7 +16,9 @@ def operand(rows, cols, l):
 A = operand(M, K, lay[0]); B = operand(K, N, lay[1])
 bias = torch.randn(N, device="cuda", dtype=torch.float16)
 C = torch.empty(M, ld8(N), device="cuda", dtype=torch.float16)[:, :N]
-for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk, multicast=mc)
+scale = (torch.rand(K, device="cuda") + 0.5) if pro == "scale_k" else None
+for _ in range(20): ge.gemm_epilogue(A, B, bias, out=C, tile_n=bn, cta_group=cg, stream_k=sk, multicast=mc,
+                                     prologue=pro, scale=scale)
 torch.cuda.synchronize()
 st = ge.debug_stats()
 lead = [s for i, s in enumerate(st) if (cg == 1 or i % 2 == 0) and s["total"] > 0]   # active leaders
@@ -24,6 +27,7 @@ tot = avg("total", lead)
 print(f"{M}x{N}x{K} {lay} bn={bn} cg={cg}: total {tot:.0f} cyc/CTA(leader)")
 for k in ("prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0", "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math", "sk_owner_wait", "sk_partial_write", "sk_pieces", "epi_end"):
     print(f"  {k:18s} {avg(k, lead):12.0f} cyc  ({100*avg(k, lead)/tot:5.1f}% of total)")
+print("  prologue transform (sum over its 4 warps): wait for stage", avg("xf_wait", lead), " rewrite", avg("xf_work", lead))
 # split-K epilogue phases (per warp lane 0, summed over the CTA's epilogue warps)
 print("  split-K: sends (sum over warps)", avg("epi_tmem_ld", lead), " owner compute+store (sum over warps)", avg("epi_math", lead))
 print("  per-CTA mma_wait_full min/max:", min(r["mma_wait_full"] for r in lead), max(r["mma_wait_full"] for r in lead))

@@ -1,14 +1,17 @@
 """Dev tool: GPU time per launch (CUDA-graph replay of 20 launches, operands L2-resident unless
 --cold) for a list of shapes with the library selected by GE_LIBRARY_FILE; leading dimensions
 padded to 8 elements like bench.py.
-usage: timed_multi.py "M N K lay [bn cg]" ... [--iters N] [--cold]"""
+usage: timed_multi.py "M N K lay [bn cg]" ... [--iters N] [--cold] [--alt LAY2]
+--alt LAY2: the graph alternates launches of layout `lay` and layout LAY2 (two kernel instantiations
+back to back, like bench.py's multi-layout steps)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2006_12645_b200 as ge
 
-args = [a for a in sys.argv[1:] if not a.startswith("--")]
+alt = sys.argv[sys.argv.index("--alt") + 1] if "--alt" in sys.argv else None
+args = [a for a in sys.argv[1:] if not a.startswith("--") and a != alt]
 iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 400
 if "--iters" in sys.argv:
     args.remove(str(iters))
@@ -30,6 +33,11 @@ for spec in args:
     bn, cg = (int(f[4]), int(f[5])) if len(f) > 5 else (0, 0)
     nset = max(1, min(16, int(3 * 126e6 // max(1, 2 * (M * K + K * N))))) if cold else 1
     As, Bs = operand(M, K, lay[0], nset), operand(K, N, lay[1], nset)
+    if alt:                      # odd launches use the second layout
+        As2, Bs2 = operand(M, K, alt[0], nset), operand(K, N, alt[1], nset)
+        As = [x for pair in zip(As, As2) for x in pair]
+        Bs = [x for pair in zip(Bs, Bs2) for x in pair]
+        nset *= 2
     bias = torch.randn(N, device="cuda", dtype=torch.float16)
     C = torch.empty(M, ld8(N), device="cuda", dtype=torch.float16)[:, :N]
     G = 20
@@ -51,5 +59,7 @@ for spec in args:
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / (reps * G) * 1e-3
     pl = ge.plan(M, N, K, layouts=lay, tile_n=bn, cta_group=cg)
+    if alt:
+        spec = spec + "/" + alt
     print(f"{lib:28s} {spec:26s} {t * 1e6:8.2f} us {2 * M * N * K / t / 1e12:7.1f} TF/s  "
           f"plan {pl['tile_m']}x{pl['tile_n']} cg{pl['cta_group']} split{pl['split_k']} swap{pl['swap_ab']}", flush=True)
