@@ -571,8 +571,8 @@ def compare_torch(torch, w, stream, iters=10):
     the same rotating operand sets and the same layouts in the same order (cuBLAS picks its kernel
     per layout, so both sides switch kernels alike).
     Like-for-like alignment: when N is not a multiple of 8, the library computes the padded
-    N' = ld8(N) columns of the same padded operand storage we read, so its C rows are 16-byte
-    aligned like ours (TFLOP/s still counts the logical 2MNK)."""
+    N' = ld8(N) columns (row-major B: the same padded storage we read; column-major B: a padded
+    copy), so its C rows are 16-byte aligned like ours (TFLOP/s still counts the logical 2MNK)."""
     out = {}
     M, N, K = w.M, w.N, w.K
     fl = 2.0 * M * N * K
@@ -585,7 +585,13 @@ def compare_torch(torch, w, stream, iters=10):
         a, b = A[0], B[0]
         if pad and lay[1] == "r":
             b = torch.as_strided(b, (K, Np), (b.stride(0), 1))     # the padded storage row pitch (ld8(N))
-        return a, b                  # col-major B keeps N columns (its C rows then have ldc = N)
+        elif pad:
+            # col-major B: a copy with Np columns (made here, outside the timed region) so the
+            # library's C rows are 16-byte aligned like ours
+            bp = torch.zeros((Np, b.stride(1)), dtype=b.dtype, device=b.device)
+            bp[:N] = torch.as_strided(b, (N, b.stride(1)), (b.stride(1), 1))
+            b = bp[:, :K].t()
+        return a, b
 
     def t(fn, it=iters):
         """One CUDA graph of `it` calls rotating the operand sets, replayed once (our protocol)."""

@@ -124,13 +124,16 @@ typedef struct {
                                        stride_prologue_tile * 2 multiples of 16 (else GE_ERR_MISALIGNED) */
     int64_t ld_prologue_tile;       /* leading dimension of S in elements (0 = packed: K row-major, M col-major) */
     int64_t stride_prologue_tile;   /* batched: element stride between items' S (0 = one S shared by all) */
+    int32_t tile_m;                 /* 0 = heuristic; 128 = 128-row tiles (with cta_group 2: HALF-ROW CTA
+                                       pairs, cta_group::2 with M = 128, 64 rows per CTA, tile_n 128/256);
+                                       256 = CTA-pair tiles of 256 rows */
     int32_t swap_ab;                /* 0 = heuristic; 1 = never; 2 = always where legal.  Swap-AB computes
                                        C^T = B^T A^T (the long N side becomes the 128-row MMA side, the
                                        skinny M side the MMA N) and stores C transposed; used for skinny
                                        M (<= 64) with ROW/COL/no bias, no prologue, no sum of matmuls
                                        (DESIGN.md "Skinny shapes").  Results stay within the bound; the
                                        summation order may differ from the unswapped launch. */
-} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0, NULL, 0, 0, 0} */
+} ge_options;                       /* NULL options = {ROW, 0, NONE, NULL, F16, 0, 0, 0, NULL, 0, 0, NULL, 0, 0, 0, 0} */
 
 typedef enum {
     GE_OK = 0,

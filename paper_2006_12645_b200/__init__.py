@@ -54,7 +54,7 @@ class GEOptions(ctypes.Structure):
                 ("cta_group", ctypes.c_int32), ("stream_k", ctypes.c_int32), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_int64), ("multicast", ctypes.c_int32),
                 ("prologue_tile", ctypes.c_void_p), ("ld_prologue_tile", ctypes.c_int64),
-                ("stride_prologue_tile", ctypes.c_int64), ("swap_ab", ctypes.c_int32)]
+                ("stride_prologue_tile", ctypes.c_int64), ("tile_m", ctypes.c_int32), ("swap_ab", ctypes.c_int32)]
 
 
 class GEPlanInfo(ctypes.Structure):
@@ -167,12 +167,12 @@ _opt_cache = {}
 
 
 def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, stream_k=0, ws=None, multicast=0,
-             tile=None, swap_ab=0):
+             tile=None, swap_ab=0, tile_m=0):
     """ge_options for these arguments; reused across calls with the same ones (per-call host cost).
     tile: (ptr, ld, batch stride) of the Hadamard prologue operand S."""
     key = (bias_mode, ldbias, prologue, scale.data_ptr() if scale is not None else 0, out_dtype, tile_n,
            cta_group, stream_k, ws.data_ptr() if ws is not None else 0, ws.numel() if ws is not None else 0,
-           multicast, tile, swap_ab)
+           multicast, tile, swap_ab, tile_m)
     o = _opt_cache.get(key)
     if o is not None:
         return o
@@ -191,6 +191,7 @@ def _options(bias_mode, ldbias, prologue, scale, out_dtype, tile_n, cta_group, s
     o.cta_group = int(cta_group)
     o.multicast = int(multicast)
     o.swap_ab = int(swap_ab)
+    o.tile_m = int(tile_m)
     if len(_opt_cache) > 512:
         _opt_cache.clear()
     _opt_cache[key] = o
@@ -311,7 +312,7 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
                   bias_mode: str = "row", prologue: Optional[str] = None, scale: Optional[torch.Tensor] = None,
                   out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
                   cta_group: int = 0, stream_k: int = 0, multicast: int = 0, swap_ab: int = 0,
-                  stream=None) -> torch.Tensor:
+                  tile_m: int = 0, stream=None) -> torch.Tensor:
     """C = relu_add(prologue(A) @ B, bias) on the current CUDA device (fp16 in, fp32 accumulate).
 
     A: (M, K) fp16, B: (K, N) fp16, row- or column-major views.  bias: (N,) for bias_mode "row",
@@ -343,7 +344,7 @@ def gemm_epilogue(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Tensor]
     ldbias, _ = _bias_ld(bias, bias_mode)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile, swap_ab)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile, swap_ab, tile_m)
     st = lib.gemm_epilogue(M, N, K, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb,
                            bias.data_ptr() if bias is not None else None, out.data_ptr(), max(out.stride(0), N, 1),
                            _op(op, bias), ctypes.byref(o), sh)
@@ -355,7 +356,7 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
                    bias: Optional[torch.Tensor] = None, *, op: Optional[str] = None, bias_mode: str = "row",
                    out_dtype: torch.dtype = torch.float16, out: Optional[torch.Tensor] = None, tile_n: int = 0,
                    cta_group: int = 0, stream_k: int = 0, multicast: int = 0, swap_ab: int = 0,
-                  stream=None) -> torch.Tensor:
+                  tile_m: int = 0, stream=None) -> torch.Tensor:
     """Sum of matmuls (Listing 4): C = epilogue(A @ B + P @ Q) in one kernel, one TMEM
     accumulator.  A (M, K1), B (K1, N), P (M, K2), Q (K2, N); P must share A's layout (row/col
     major) and Q B's."""
@@ -379,7 +380,7 @@ def gemm2_epilogue(A: torch.Tensor, B: torch.Tensor, P: torch.Tensor, Q: torch.T
     ldbias, _ = _bias_ld(bias, bias_mode)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, None, None, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, None, swap_ab)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, None, swap_ab, tile_m)
     st = lib.gemm2_epilogue(M, N, K1, K2, la, lb, A.data_ptr(), lda, B.data_ptr(), ldb, P.data_ptr(), ldp,
                             Q.data_ptr(), ldq, bias.data_ptr() if bias is not None else None, out.data_ptr(),
                             max(out.stride(0), N, 1), _op(op, bias), ctypes.byref(o), sh)
@@ -408,7 +409,8 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
                           op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
                           scale: Optional[torch.Tensor] = None, out_dtype: torch.dtype = torch.float16,
                           out: Optional[torch.Tensor] = None, tile_n: int = 0, cta_group: int = 0,
-                          stream_k: int = 0, multicast: int = 0, swap_ab: int = 0, stream=None) -> torch.Tensor:
+                          stream_k: int = 0, multicast: int = 0, swap_ab: int = 0, tile_m: int = 0,
+                          stream=None) -> torch.Tensor:
     """Strided-batched form: A (b, M, K), B (b, K, N), bias (N,)/(b, N) [row], (M,)/(b, M) [col],
     (M, ld)/(b, M, ld) [full]; a 1-D/2-D bias is shared by every item.  One persistent launch."""
     lib = load_library()
@@ -421,7 +423,7 @@ def gemm_epilogue_batched(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch
         out = torch.empty((batch, M, N), dtype=out_dtype, device=A.device)
     sh = _stream(stream, A.get_device())
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k,
-                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile, swap_ab)
+                 _workspace(A.device, sh) if stream_k != 1 else None, multicast, tile, swap_ab, tile_m)
     st = lib.gemm_epilogue_batched(batch, M, N, K, la, lb, A.data_ptr(), lda, sA, B.data_ptr(), ldb, sB,
                                    bias.data_ptr() if bias is not None else None, sbias, out.data_ptr(),
                                    max(out.stride(1), N, 1), out.stride(0), _op(op, bias), ctypes.byref(o), sh)
@@ -433,7 +435,8 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
                        op: Optional[str] = None, bias_mode: str = "row", prologue: Optional[str] = None,
                        scale: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                        out_dtype: torch.dtype = torch.float16, tile_n: int = 0, cta_group: int = 0,
-                       stream_k: int = 0, multicast: int = 0, swap_ab: int = 0, stream=None) -> torch.Tensor:
+                       stream_k: int = 0, multicast: int = 0, swap_ab: int = 0, tile_m: int = 0,
+                          stream=None) -> torch.Tensor:
     """End-to-end path through the C ABI with HOST (CPU, ideally pinned) tensors: the library copies
     the inputs to the device, runs the fused kernel and copies C back, synchronously."""
     lib = load_library()
@@ -450,7 +453,7 @@ def gemm_epilogue_host(A: torch.Tensor, B: torch.Tensor, bias: Optional[torch.Te
                           pin_memory=A.is_pinned())
     out3 = out if out.dim() == 3 else out.unsqueeze(0)
     o = _options(bias_mode, ldbias, prologue, scale, out.dtype, tile_n, cta_group, stream_k, multicast=multicast,
-                 tile=tile, swap_ab=swap_ab)
+                 tile=tile, swap_ab=swap_ab, tile_m=tile_m)
     st = lib.gemm_epilogue_host(batch, M, N, K, la, lb, A3.data_ptr(), lda, sA, B3.data_ptr(), ldb, sB,
                                 bias.data_ptr() if bias is not None else None, sbias, out3.data_ptr(),
                                 max(out3.stride(1), N, 1), out3.stride(0), _op(op, bias), ctypes.byref(o),
@@ -466,12 +469,12 @@ def validate_args(*args) -> int:
 
 def plan(M: int, N: int, K: int, batch: int = 1, layouts: str = "rr", num_sms: int = 148, tile_n: int = 0,
          cta_group: int = 0, stream_k: int = 0, prologue: Optional[str] = None, multicast: int = 0,
-         swap_ab: int = 0, op: str = "bias_relu", bias_mode: str = "row") -> dict:
+         swap_ab: int = 0, op: str = "bias_relu", bias_mode: str = "row", tile_m: int = 0) -> dict:
     """The launch configuration the library's planner picks (ge_plan_ex), assuming a stream-K
     workspace is passed (the device entry points of this binding always pass one)."""
     lib = load_library()
     o = _options(bias_mode, 0, prologue, None, torch.float16, tile_n, cta_group, stream_k, multicast=multicast,
-                 swap_ab=swap_ab)
+                 swap_ab=swap_ab, tile_m=tile_m)
     info = GEPlanInfo()
     st = lib.ge_plan_ex(batch, M, N, K, 0 if layouts[0] == "r" else 1, 0 if layouts[1] == "r" else 1,
                         _op(op, True), ctypes.byref(o), num_sms, ctypes.byref(info))

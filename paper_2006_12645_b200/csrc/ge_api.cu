@@ -133,6 +133,12 @@ ge_status validate_options(const Args& a) {
                              (o.tile_n && o.tile_n != 256 && o.tile_n != 512)))
         return fail(GE_ERR_INVALID_VALUE, "multicast = 2 needs no prologue, stream_k != 2, cta_group 0/2, tile_n 0/256/512");
     if (o.swap_ab < 0 || o.swap_ab > 2) return fail(GE_ERR_INVALID_VALUE, "swap_ab must be 0, 1 or 2");
+    if (o.tile_m != 0 && o.tile_m != 128 && o.tile_m != 256) return fail(GE_ERR_INVALID_VALUE, "tile_m must be 0, 128 or 256");
+    if (o.tile_m == 256 && o.cta_group == 1) return fail(GE_ERR_INVALID_VALUE, "tile_m 256 needs cta_group 2");
+    if (o.tile_m == 128 && o.cta_group == 2 &&
+        (o.tile_n == 64 || o.tile_n == 192 || o.tile_n == 512 || o.multicast == 2 || o.stream_k == 2))
+        return fail(GE_ERR_INVALID_VALUE,
+                    "half-row pair tiles (tile_m 128, cta_group 2) take tile_n 0/128/256, no multicast, no forced stream-K");
     if (o.workspace_bytes < 0 || (o.workspace && (reinterpret_cast<uintptr_t>(o.workspace) & 15)))
         return fail(GE_ERR_INVALID_VALUE, "workspace must be 16-byte aligned with a non-negative size");
     return GE_OK;
@@ -252,6 +258,7 @@ struct Plan {
     int64_t sk_tiles;      // tiles of the last, partial wave split stream-K across all clusters (0 = none)
     int64_t clusters;      // persistent clusters launched
     int splits = 0;        // split-K: clusters per tile (0 = off; then clusters = tiles * splits)
+    bool hr = false;       // half-row CTA pair: tile 128 x bn, 64 rows per CTA (cta_group::2, M = 128)
 };
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -283,6 +290,16 @@ constexpr double kDrain512 = 13600.0;   // cycles exposed per 256 x 512 pair til
 double config_eff(int bn, int cg) {
     if (cg == 2) return bn == 512 ? 1.32 : bn == 256 ? 1.10 : bn == 192 ? 0.87 : 0.59;
     return bn == 256 ? 0.92 : bn == 192 ? 0.82 : bn == 128 ? 0.60 : 0.29;
+}
+// Half-row pair tiles (128 x BN, 64 rows per CTA), relative to the same per-SM reference; GE_HR_EFF
+// overrides (calibration only).
+double config_eff_hr(int bn) {
+    static const double env = [] {
+        const char* e = getenv("GE_HR_EFF");
+        return e ? atof(e) : 0.0;
+    }();
+    if (env > 0) return env;
+    return bn == 256 ? 0.20 : 0.20;     // provisional (not picked by default until calibrated on B200)
 }
 // Cycles per tile column exposed once per launch by the last tile's drain (TMEM -> registers ->
 // smem -> TMA store runs after the final MMA; wider tiles drain longer), same refit.
@@ -343,6 +360,7 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap, bool sk_allowed) {
         const int bn = c[0], cg = c[1];
         if (a.o.tile_n && a.o.tile_n != bn) continue;
         if (a.o.cta_group && a.o.cta_group != cg) continue;
+        if (a.o.tile_m && a.o.tile_m != 128 * cg) continue;             // (tile_m 128 with pairs: half-row, below)
         if (bn == 192 && cg == 2 && a.lb == GE_ROW_MAJOR) continue;     // pair tile needs a K-major B
         // Skinny M (<= 64 rows): most of every A stage is TMA zero-fill, the shape is HBM bound on B
         // and 128 x 128 tiles measure best (profiles/r01_tune_sweep.json); narrower tiles only add
@@ -419,11 +437,36 @@ Plan make_plan(const Args& a, int sms, const SplitCap* cap, bool sk_allowed) {
             best_cost = cost;
         }
     }
+    // Half-row CTA pairs: 128 x BN tiles with 64 rows per CTA
+    // (cta_group::2, M = 128).  Per CTA and k-block the MMA reads a 64-row A slice and its half of B,
+    // so narrow tiles keep the tensor pipe fed where 128-row single-CTA tiles re-read A from smem
+    // for every N = 64..128 instruction.  Data-parallel tiles only.
+    const bool hr_ok = a.o.multicast != 2 && a.o.stream_k != 2 && (!a.o.cta_group || a.o.cta_group == 2) &&
+                       (!a.o.tile_m || a.o.tile_m == 128);
+    if (hr_ok) {
+        for (const int bn : {256, 128}) {
+            if (a.o.tile_n && a.o.tile_n != bn) continue;
+            const int64_t tiles = a.batch * cdiv(a.M, 128) * cdiv(a.N, bn);
+            const int64_t conc = std::max(1, sms / 2);
+            double eff = config_eff_hr(bn);
+            if (a.o.prologue != GE_PRO_NONE) eff *= 0.55;
+            const double t_kb = 64.0 * bn * 64 * 2 / (8192.0 * eff);
+            const double waves = static_cast<double>(cdiv(std::max<int64_t>(tiles, 1), conc));
+            const double cost = waves * nkb * t_kb + kDrainPerCol * bn / 2;
+            if (best.bn == 0 || cost < best_cost * (1 - 1e-9)) {
+                best = Plan{bn, 2, ge::stages_for(bn, 2, a.o.prologue == GE_PRO_HADAMARD, true), false, tiles, 0,
+                            std::min<int64_t>(tiles, conc)};
+                best.hr = true;
+                best_cost = cost;
+            }
+        }
+    }
     // Multicast clusters of two CTA pairs: data-parallel tiles of
     // 512 x BN, co-resident clusters from cudaOccupancyMaxActiveClusters (GPC-bound: 4-CTA clusters
     // leave some SMs idle, which the cost model charges through `conc`).
     const bool mc_ok = a.o.multicast != 1 && a.o.prologue == GE_PRO_NONE && a.o.stream_k != 2 &&
-                       (!a.o.cta_group || a.o.cta_group == 2) && (a.M > 256 || a.o.multicast == 2);
+                       (!a.o.cta_group || a.o.cta_group == 2) && (a.M > 256 || a.o.multicast == 2) &&
+                       a.o.tile_m != 128;
     if (mc_ok) {
         for (const int bn : {512, 256}) {
             if (a.o.tile_n && a.o.tile_n != bn) continue;
@@ -595,12 +638,12 @@ bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, int es, const void* ptr, i
 // would hold only M valid rows (a shallow ring of useful B bytes, a split-K reduction of mostly zeros).
 bool swap_legal(const Args& a) {
     return a.o.prologue == GE_PRO_NONE && a.K2 == 0 && !(has_bias(a.op) && a.o.bias_mode == GE_BIAS_FULL) &&
-           a.o.multicast != 2 && a.o.stream_k != 2 && a.o.cta_group != 2 && a.o.tile_n != 512;
+           a.o.multicast != 2 && a.o.stream_k != 2 && a.o.cta_group != 2 && a.o.tile_n != 512 && a.o.tile_m != 256;
 }
 bool use_swap(const Args& a) {
     if (a.o.swap_ab == 1 || !swap_legal(a)) return false;
     if (a.o.swap_ab == 2) return true;
-    return a.M <= 64 && a.N >= 1024 && !a.o.tile_n && !a.o.cta_group;
+    return a.M <= 64 && a.N >= 1024 && !a.o.tile_n && !a.o.cta_group && !a.o.tile_m;
 }
 // The swapped problem: A' = B^T (M' = N), B' = A^T (N' = M); a transposed view flips the layout
 // bit and keeps the leading dimension; the bias modes ROW (bias[j]) and COL (bias[i]) trade places.
@@ -659,7 +702,8 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
     std::memset(&maps, 0, sizeof maps);
     if (a.K > 0) {
         bool ok;
-        if (!a_mn) ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.K, a.M, a.batch, a.lda, a.sA, 64, 128);
+        const uint32_t arows = pl.hr ? 64 : 128;                       // A rows per CTA (the K-major box)
+        if (!a_mn) ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.K, a.M, a.batch, a.lda, a.sA, 64, arows);
         else ok = encode3d(&maps.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.A, a.M, a.K, a.batch, a.lda, a.sA, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for A");
         // B rows per MMA per CTA; multicast clusters load (and multicast) half of them per CTA
@@ -673,14 +717,14 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
         const int64_t sT = a.batch > 1 ? a.o.stride_prologue_tile : 0;
         bool ok;
         if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.o.prologue_tile, a.K, a.M,
-                                 sT ? a.batch : 1, a.o.ld_prologue_tile, sT, 64, 128);
+                                 sT ? a.batch : 1, a.o.ld_prologue_tile, sT, 64, pl.hr ? 64 : 128);
         else ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.o.prologue_tile, a.M, a.K,
                            sT ? a.batch : 1, a.o.ld_prologue_tile, sT, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the prologue tile");
     }
     if (a.K2 > 0) {
         bool ok;
-        if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.K2, a.M, 1, a.ldp, 0, 64, 128);
+        if (!a_mn) ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.K2, a.M, 1, a.ldp, 0, 64, pl.hr ? 64 : 128);
         else ok = encode3d(&maps.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.P, a.M, a.K2, 1, a.ldp, 0, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for P");
         const uint32_t brows = static_cast<uint32_t>(std::min(pl.bn, 256) / pl.cg / (pl.mc ? 2 : 1));
@@ -701,7 +745,7 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
     p.N = static_cast<int>(a.N);
     p.K = static_cast<int>(a.K);
     p.batch = static_cast<int>(a.batch);
-    p.num_m_tiles = static_cast<int>(cdiv(a.M, 128 * pl.cg * (pl.mc ? 2 : 1)));
+    p.num_m_tiles = static_cast<int>(cdiv(a.M, pl.hr ? 128 : 128 * pl.cg * (pl.mc ? 2 : 1)));
     p.num_n_tiles = static_cast<int>(cdiv(a.N, pl.bn));
     p.a_mn = a_mn ? 1 : 0;
     p.b_mn = b_mn ? 1 : 0;
@@ -767,7 +811,10 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
     }
     const int grid = static_cast<int>(std::max<int64_t>(plan.clusters, 1) * plan.cg * (plan.mc ? 2 : 1));
     cudaError_t e;
-    if (pl.mc) {
+    if (pl.hr) {
+        if (pl.bn == 128) e = ge::launch_cg2_bn128_hr(f32, pro, maps, p, grid, st);
+        else e = ge::launch_cg2_bn256_hr(f32, pro, maps, p, grid, st);
+    } else if (pl.mc) {
         if (pl.bn == 512) e = ge::launch_cg2_bn512_mc(f32, pro, maps, p, grid, st);
         else e = ge::launch_cg2_bn256_mc(f32, pro, maps, p, grid, st);
     } else if (pl.cg == 1) {
@@ -794,7 +841,7 @@ Args make_args(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t la, int32
                int64_t ldc, int64_t sC, int32_t op, const ge_options* opt) {
     Args a{batch, M, N, K, la, lb, A, lda, sA, B, ldb, sB, bias, sBias, C, ldc, sC, op, {}};
     if (opt) a.o = *opt;
-    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0, nullptr, 0, 0, 0};
+    else a.o = ge_options{GE_BIAS_ROW, 0, GE_PRO_NONE, nullptr, GE_OUT_F16, 0, 0, 0, nullptr, 0, 0, nullptr, 0, 0, 0, 0};
     return a;
 }
 
@@ -841,7 +888,8 @@ int clusters_cg1(int bn, int cluster) {
          : bn == 192 ? clusters_cg1_bn192(cluster) : clusters_cg1_bn256(cluster);
 }
 template <bool SX>
-int smem_bytes_t(int bn, int cg) {
+int smem_bytes_t(int bn, int cg, bool hr) {
+    if (hr) return bn == 128 ? Cfg<128, 2, SX, true>::kSmemBytes : Cfg<256, 2, SX, true>::kSmemBytes;
     if (cg == 1)
         return bn == 64 ? Cfg<64, 1, SX>::kSmemBytes : bn == 128 ? Cfg<128, 1, SX>::kSmemBytes
              : bn == 192 ? Cfg<192, 1, SX>::kSmemBytes : Cfg<256, 1, SX>::kSmemBytes;
@@ -849,15 +897,18 @@ int smem_bytes_t(int bn, int cg) {
          : bn == 256 ? Cfg<256, 2, SX>::kSmemBytes : Cfg<512, 2, SX>::kSmemBytes;
 }
 template <bool SX>
-int stages_t(int bn, int cg) {
+int stages_t(int bn, int cg, bool hr) {
+    if (hr) return bn == 128 ? Cfg<128, 2, SX, true>::kStages : Cfg<256, 2, SX, true>::kStages;
     if (cg == 1)
         return bn == 64 ? Cfg<64, 1, SX>::kStages : bn == 128 ? Cfg<128, 1, SX>::kStages
              : bn == 192 ? Cfg<192, 1, SX>::kStages : Cfg<256, 1, SX>::kStages;
     return bn == 128 ? Cfg<128, 2, SX>::kStages : bn == 192 ? Cfg<192, 2, SX>::kStages
          : bn == 256 ? Cfg<256, 2, SX>::kStages : Cfg<512, 2, SX>::kStages;
 }
-int smem_bytes_for(int bn, int cg, bool sx) { return sx ? smem_bytes_t<true>(bn, cg) : smem_bytes_t<false>(bn, cg); }
-int stages_for(int bn, int cg, bool sx) { return sx ? stages_t<true>(bn, cg) : stages_t<false>(bn, cg); }
+int smem_bytes_for(int bn, int cg, bool sx, bool hr) {
+    return sx ? smem_bytes_t<true>(bn, cg, hr) : smem_bytes_t<false>(bn, cg, hr);
+}
+int stages_for(int bn, int cg, bool sx, bool hr) { return sx ? stages_t<true>(bn, cg, hr) : stages_t<false>(bn, cg, hr); }
 }  // namespace ge
 
 extern "C" {
@@ -1111,7 +1162,7 @@ ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layout
     }
     // descriptive: assumes the caller will pass a workspace of *workspace_bytes when stream-K is planned
     const Plan p = make_plan(a, num_sms, split_capacity(), true);     // (nullptr without a device)
-    if (tile_m) *tile_m = 128 * p.cg * (p.mc ? 2 : 1);
+    if (tile_m) *tile_m = p.hr ? 128 : 128 * p.cg * (p.mc ? 2 : 1);
     if (tile_n) *tile_n = p.bn;
     if (cta_group) *cta_group = p.cg;
     if (stages) *stages = p.stages;
@@ -1136,7 +1187,7 @@ ge_status ge_plan_ex(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t lay
     const bool sw = use_swap(a);
     const Args t = sw ? swapped(a) : a;
     const Plan p = make_plan(t, num_sms, split_capacity(), true);
-    out->tile_m = 128 * p.cg * (p.mc ? 2 : 1);
+    out->tile_m = p.hr ? 128 : 128 * p.cg * (p.mc ? 2 : 1);
     out->tile_n = p.bn;
     out->cta_group = p.cg;
     out->stages = p.stages;

@@ -155,15 +155,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // SX: the Hadamard prologue's S tile is staged like A (same box, same swizzle) in its own ring slot.
-template <int BN, int CG, bool SX = false>
+// HR: half-row CTA pairs (cta_group::2 with M = 128: 64 rows per CTA, DESIGN.md "Half-row pair
+// tiles"): each CTA stages a 64-row A block and half of B, and its 64 x BN accumulator occupies all
+// 128 TMEM lanes over BN/2 columns (columns [0, BN/2) in lanes 0-63, [BN/2, BN) in lanes 64-127).
+template <int BN, int CG, bool SX = false, bool HR = false>
 struct Cfg {
-    static constexpr int kTileM = kRowsPerCta * CG;
+    static constexpr int kRows = HR ? 64 : kRowsPerCta;                // A rows (tile rows) per CTA
+    static constexpr int kBNT = HR ? BN / 2 : BN;                     // TMEM columns per accumulator
+    static constexpr int kTileM = kRows * CG;
     static constexpr int kUmmaN = BN < 256 ? BN : 256;                // N of one tcgen05.mma
     static constexpr int kNHalves = BN / kUmmaN;                      // MMAs per K step (BN = 512: 2)
     static constexpr int kBBlockRows = kUmmaN / CG;                   // B rows per CTA per MMA
     static constexpr int kBBlockBytes = kBBlockRows * kBK * 2;
     static constexpr int kBRows = BN / CG;                            // B rows (N) staged per CTA
-    static constexpr int kAStage = kRowsPerCta * kBK * 2;             // 16 KB
+    static constexpr int kAStage = kRows * kBK * 2;                   // 16 KB (8 KB half-row)
     static constexpr int kBStage = kBRows * kBK * 2;
     static constexpr int kSStage = SX ? kAStage : 0;
     static constexpr int kStageBytes = kAStage + kBStage + kSStage;
@@ -180,8 +185,8 @@ struct Cfg {
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStagingBytes + kBiasBytes + kBarBytes;
     // fp32 accumulator in TMEM: double-buffered when two fit in the 512 columns, else one buffer
     // drained half by half (per-half barriers let the next tile's first MMAs start early).
-    static constexpr int kAccStages = 2 * BN <= 512 ? 2 : 1;
-    static constexpr int kTmemUsed = kAccStages * BN;
+    static constexpr int kAccStages = 2 * kBNT <= 512 ? 2 : 1;
+    static constexpr int kTmemUsed = kAccStages * kBNT;
     // tcgen05.alloc takes a power of two >= 32 columns
     static constexpr int kTmemCols = kTmemUsed <= 32 ? 32 : kTmemUsed <= 64 ? 64 : kTmemUsed <= 128 ? 128
                                    : kTmemUsed <= 256 ? 256 : 512;
@@ -191,6 +196,7 @@ struct Cfg {
     static_assert(kSmemBytes <= kSmemBudget, "smem overflow");
     static_assert(BN == 64 || BN == 128 || BN == 192 || BN == 256 || (BN == 512 && CG == 2), "BN");
     static_assert(kTmemUsed <= 512, "TMEM");
+    static_assert(!HR || (CG == 2 && BN <= 256 && BN >= 128), "half-row tiles are CTA pairs with BN 128 / 256");
 };
 
 __device__ __forceinline__ void decode_tile(const Params& p, long long t, int tile_m, int& b, int& mt, int& nt) {
@@ -319,13 +325,13 @@ __host__ __device__ constexpr int kernel_threads(bool out_f32, bool pro) {
 // Hadamard tile S staged by TMA next to A (its second input dataspace).
 // The operand layouts (K- or MN-major A and B) are runtime parameters (Params::a_mn / b_mn): one
 // instantiation serves the four layout pairs, so a step that alternates layouts runs one kernel.
-template <int BN, bool OUT_F32, int PRO, int CG, bool MC = false>
+template <int BN, bool OUT_F32, int PRO, int CG, bool MC = false, bool HR = false>
 __global__ void __launch_bounds__(kernel_threads(OUT_F32, PRO != 0), 1)
 ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_p,
                 const __grid_constant__ CUtensorMap tmap_q, const Params p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-    using C_ = Cfg<BN, CG, PRO == 2>;
+    using C_ = Cfg<BN, CG, PRO == 2, HR>;
     constexpr int S = C_::kStages;
     constexpr int W = 32;                                // output columns per epilogue chunk (one tcgen05.ld)
     constexpr int NCHUNK = BN / W;
@@ -334,7 +340,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     constexpr int HALF_COLS = BN / NH;
     constexpr bool kPairAcq = GE_PAIR_ACQ && !PRO && NH == 1 && !MC && GE_PAIR_RELEASE;
     const bool A_MN = p.a_mn != 0, B_MN = p.b_mn != 0;       // MN-major (row-major B / col-major A)
-    const uint32_t IDESC = ptx::make_idesc_f16(kRowsPerCta * CG, C_::kUmmaN, A_MN, B_MN);
+    const uint32_t IDESC = ptx::make_idesc_f16(C_::kRows * CG, C_::kUmmaN, A_MN, B_MN);
 
     const unsigned long long g_entry = GE_DBG ? globaltimer() : 0ull;
     extern __shared__ uint8_t smem_raw[];
@@ -432,7 +438,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const long long t = pc.tile;
                 int b, mt, nt;
                 decode_tile(p, t, TILE_M, b, mt, nt);
-                const int m0 = mt * TILE_M + pair * C_::kTileM + rank * kRowsPerCta;
+                const int m0 = mt * TILE_M + pair * C_::kTileM + rank * C_::kRows;
                 const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                     // paired release: the MMA warp commits only the odd stage of each pair (that
@@ -477,7 +483,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     auto load_a = [&](uint8_t* dst, const CUtensorMap* map, int cb) {
                         if (A_MN) {
 #pragma unroll
-                            for (int i = 0; i < kRowsPerCta / 64; ++i) load(dst + i * 8192, map, m0 + i * 64, k0, pol_a, cb);
+                            for (int i = 0; i < C_::kRows / 64; ++i) load(dst + i * 8192, map, m0 + i * 64, k0, pol_a, cb);
                         } else {
                             load(dst, map, k0, m0, pol_a, cb);
                         }
@@ -534,7 +540,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const Piece pc = work.get(it);
                 const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
                 const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + acc * C_::kBNT;
                 if (dbg && lane == 0 && it == 0) dl[DBG_FIRST_MMA] = static_cast<unsigned long long>(clock64() - t_start);
                 // K-major: +32 B per K=16 step inside the 128-B swizzle row; SBO = 8 rows x 128 B.
                 // MN-major: +16 rows x 128 B per step; LBO = next 64-wide MN atom (64 x 128 B),
@@ -668,7 +674,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         constexpr int STG = 32 * ROWB;                           // one staging buffer (32 rows)
         constexpr int NV = ROWB / 16;                            // 16-B vectors per row
         constexpr int NWORD = ROWB / 4;                          // 32-bit words per row
-        constexpr int CPH_ALL = HALF_COLS / W;                   // 32-column chunks per accumulator half
+        constexpr int CPH_ALL = (HR ? C_::kBNT : HALF_COLS) / W;  // 32-column TMEM chunks per accumulator half
+        // half-row pairs: lanes 64-127 hold tile columns [BN/2, BN) (a chunk offset for quarters 2, 3)
+        const int qc = HR ? (q >> 1) * (C_::kBNT / W) : 0;
         constexpr int CPH = CPH_ALL / NG;                        // ... owned by this warp
         // Single-buffered accumulator (BN = 512), fp16 out: compute all of this warp's chunks of a
         // half into packed registers first and release the half before any store, so the next
@@ -690,7 +698,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             decode_tile(p, t, TILE_M, b, mt, nt);
             const int acc = (C_::kAccStages == 2) ? (it & 1) : 0;
             const uint32_t acc_phase = (C_::kAccStages == 2) ? ((it >> 1) & 1) : (it & 1);
-            const int row0 = mt * TILE_M + pair * C_::kTileM + rank * kRowsPerCta + q * 32;   // first row of this warp
+            const int row0 = mt * TILE_M + pair * C_::kTileM + rank * C_::kRows + (HR ? (q & 1) : q) * 32;   // first row of this warp
             const int row = row0 + lane;
             const __half* bias_b = p.bias ? p.bias + b * p.stride_bias : nullptr;
             // Bias operands are fetched while this tile's MMAs still run (global loads would miss
@@ -724,7 +732,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             };
             if (nkb > 0) wait_acc();
             const long long t_epi0 = (dbg && e_idx == 0) ? clock64() : 0;
-            const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+            const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C_::kBNT;
 
             // TMEM columns of chunk c -> registers (zeros when K == 0)
             auto load = [&](const int c, uint32_t* v) {
@@ -752,7 +760,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             // max(v, +0) (-0 and NaN -> +0, R-C5), one RNE pack per two outputs.  The last tile's
             // drain is exposed on single-wave shapes and was instruction-fetch bound (ncu: no_inst)
             // with the general code inline, so it also gets its own chunk loop below.
-            auto compute_fast = [&](const int c, const uint32_t* v, uint32_t* w) {
+            auto compute_fast = [&](const int ct, const uint32_t* v, uint32_t* w) {
+                const int c = ct + qc;                               // tile column chunk
                 uint32_t r[W];
                 if (p.bias_mode == BIAS_COL) {
                     const float bc = p.bias_sign * beta_col;
@@ -794,11 +803,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
             };
             // S2 of Listing 1: v = acc + beta, relu, one RNE conversion; packed into NWORD words
-            auto compute = [&](const int c, const uint32_t* v, uint32_t* w) {
+            auto compute = [&](const int ct, const uint32_t* v, uint32_t* w) {
                 if (GE_EPI_FAST && epi_fast) {
-                    compute_fast(c, v, w);
+                    compute_fast(ct, v, w);
                     return;
                 }
+                const int c = ct + qc;                               // tile column chunk
                 const int col0 = nt * BN + c * W;
                 const float bsg = p.bias_sign;
                 float f[W];
@@ -877,8 +887,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 }
             };
             // packed row of chunk c -> C (TMA store through a swizzled staging chunk, or st.global)
-            auto store = [&](const int c, const uint32_t* w) {
-                const int col0 = nt * BN + c * W;
+            auto store = [&](const int ct, const uint32_t* w) {
+                const int col0 = nt * BN + (ct + qc) * W;
                 if (p.c_tma) {
                     // The swizzle matches the C tensor map: 128-B rows use SWIZZLE_128B (16-B chunk
                     // ^= row % 8), 64-B rows SWIZZLE_64B (chunk ^= (row / 2) % 4); both are

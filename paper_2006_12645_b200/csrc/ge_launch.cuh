@@ -14,15 +14,15 @@ struct Maps {
     CUtensorMap a, b, c, p, q;      // p, q: second matmul of a sum of matmuls (unused otherwise)
 };
 
-// Smem bytes / ring stages of the (BN, CG) configuration, sx: with the Hadamard S stage (host and
-// device agree through Cfg).
-int smem_bytes_for(int bn, int cg, bool sx = false);
-int stages_for(int bn, int cg, bool sx = false);
+// Smem bytes / ring stages of the (BN, CG) configuration, sx: with the Hadamard S stage, hr: half-row
+// CTA pairs (host and device agree through Cfg).
+int smem_bytes_for(int bn, int cg, bool sx = false, bool hr = false);
+int stages_for(int bn, int cg, bool sx = false, bool hr = false);
 
-template <int BN, bool OUT_F32, int PRO, int CG, bool MC = false>
+template <int BN, bool OUT_F32, int PRO, int CG, bool MC = false, bool HR = false>
 cudaError_t launch_one(const Maps& m, const Params& p, int grid, cudaStream_t st) {
-    auto kern = ge_fused_kernel<BN, OUT_F32, PRO, CG, MC>;
-    constexpr int smem = Cfg<BN, CG, PRO == 2>::kSmemBytes;
+    auto kern = ge_fused_kernel<BN, OUT_F32, PRO, CG, MC, HR>;
+    constexpr int smem = Cfg<BN, CG, PRO == 2, HR>::kSmemBytes;
     static bool attr_done = false;   // benign race: setting the attribute twice is harmless
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -86,13 +86,13 @@ int max_active_clusters(int cluster) {
 // Dispatch over the 6 (OUT_F32, PRO in {0, 1, 2}) variants of one (BN, CG) configuration; the operand
 // layouts travel in Params (a_mn / b_mn), and the host rejects the one unsupported layout (BN = 192
 // CTA pairs stage 96 B rows per CTA: K-major B only, ge_api.cu validate()).
-template <int BN, int CG, bool MC = false>
+template <int BN, int CG, bool MC = false, bool HR = false>
 cudaError_t launch_bn_cg(bool f32, int pro, const Maps& m, const Params& p, int grid, cudaStream_t st) {
     switch ((f32 ? 3 : 0) + pro) {
 #define GE_CASE(F, P)                                                             \
     case (F ? 3 : 0) + P:                                                         \
         if constexpr (MC && P) return cudaErrorInvalidValue;                      \
-        else return launch_one<BN, F, P, CG, MC>(m, p, grid, st);
+        else return launch_one<BN, F, P, CG, MC, HR>(m, p, grid, st);
         GE_CASE(false, 0)
         GE_CASE(false, 1)
         GE_CASE(false, 2)
@@ -120,6 +120,8 @@ cudaError_t launch_cg2_bn256(bool, int, const Maps&, const Params&, int, cudaStr
 cudaError_t launch_cg2_bn512(bool, int, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn512_mc(bool, int, const Maps&, const Params&, int, cudaStream_t);
 cudaError_t launch_cg2_bn256_mc(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn128_hr(bool, int, const Maps&, const Params&, int, cudaStream_t);
+cudaError_t launch_cg2_bn256_hr(bool, int, const Maps&, const Params&, int, cudaStream_t);
 int clusters_mc(int bn);     // co-resident 4-CTA multicast clusters of the (bn, pair) kernel
 
 }  // namespace ge

@@ -768,3 +768,79 @@ def test_swap_ab_batched_padding_and_default():
     unswapped = ge.gemm_epilogue_batched(A, B, bias, swap_ab=1)
     torch.cuda.synchronize()
     assert torch.equal(unswapped, Cbuf[:, :, :N])          # exact data: both orders agree bitwise
+
+
+# ------------------------------------------------------------------ half-row CTA pairs (tile_m 128, cta_group 2)
+@pytest.mark.parametrize("tile_n", [128, 256])
+@pytest.mark.parametrize("layouts", workloads.LAYOUTS)
+def test_half_row_pairs_exact_and_bound(tile_n, layouts):
+    """cta_group::2 with M = 128 (64 rows per CTA; the accumulator's columns [BN/2, BN) live in TMEM
+    lanes 64-127): bitwise on small integers (fp16 and fp32 out) and within the bound + ReLU
+    invariant on uniform data, with M/N/K tails (333 x 777 x 321: a partial last row tile of 77 rows,
+    i.e. one CTA of the pair with 13 valid rows)."""
+    assert ge.plan(333, 777, 321, layouts=layouts, tile_n=tile_n, cta_group=2, tile_m=128)["tile_m"] == 128
+    for kind in ("smallint", "uniform"):
+        prob = workloads.make_problem(333, 777, 321, seed=140, kind=kind, bias_mode="row")
+        for dt in (torch.float16, torch.float32):
+            got = run_gpu(prob, layouts, out_dtype=dt, tile_n=tile_n, cta_group=2, tile_m=128)
+            pre, mag = oracle_run(prob, layouts, relu=False)
+            out = np.where(pre > 0, pre, 0.0)
+            if kind == "smallint":
+                assert np.array_equal(got, exact_expect(out, dt)), (tile_n, layouts, dt)
+            else:
+                check_bound(got, out, mag, f"half-row {tile_n} {layouts}")
+                check_relu_invariant(got, pre, mag, f"half-row {tile_n} {layouts}")
+
+
+@pytest.mark.parametrize("variant", ["col_bias", "full_bias", "prologue_scale", "prologue_relu", "hadamard", "batched",
+                                     "odd", "k0", "gemm2", "literal"])
+def test_half_row_pairs_variants(variant):
+    """The half-row pair tile through the other epilogue / prologue / batch paths, bitwise on small
+    integers."""
+    kw = dict(tile_n=128, cta_group=2, tile_m=128)
+    if variant in ("col_bias", "full_bias"):
+        bm = "col" if variant == "col_bias" else "full"
+        prob = workloads.make_problem(300, 264, 200, seed=141, kind="smallint", bias_mode=bm)
+        got = run_gpu(prob, "rc", **kw)
+        out, _ = oracle_run(prob, "rc")
+        assert np.array_equal(got, exact_expect(out, torch.float16))
+    elif variant.startswith("prologue") or variant == "hadamard":
+        pro = {"prologue_scale": "scale_k", "prologue_relu": "relu", "hadamard": "hadamard"}[variant]
+        for lay in ("rr", "cc"):
+            prob = workloads.make_problem(257, 300, 200, seed=142, kind="smallint", bias_mode="row", prologue=pro)
+            got = run_gpu(prob, lay, tile_n=256, cta_group=2, tile_m=128)
+            out, _ = oracle_run(prob, lay)
+            assert np.array_equal(got, exact_expect(out, torch.float16)), (variant, lay)
+    elif variant == "batched":
+        probs = [workloads.make_problem(200, 136, 96, seed=143 + b, kind="smallint", bias_mode="row") for b in range(3)]
+        A = torch.stack([p.A for p in probs]).cuda()
+        B = torch.stack([p.B for p in probs]).cuda()
+        bias = torch.stack([p.bias for p in probs]).cuda()
+        C = ge.gemm_epilogue_batched(A, B, bias, **kw)
+        torch.cuda.synchronize()
+        for b, p in enumerate(probs):
+            out, _ = oracle_run(p, "rr")
+            assert np.array_equal(C[b].float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+    elif variant == "odd":
+        for (M, N, K) in ((1, 1, 1), (65, 129, 17), (127, 255, 64), (129, 8, 1000)):
+            prob = workloads.make_problem(M, N, K, seed=147, kind="smallint", bias_mode="row")
+            got = run_gpu(prob, "rr", **kw)
+            out, _ = oracle_run(prob, "rr")
+            assert np.array_equal(got, exact_expect(out, torch.float16)), (M, N, K)
+    elif variant == "k0":
+        prob = workloads.make_problem(70, 90, 0, seed=148, bias_mode="col")
+        got = run_gpu(prob, "rr", **kw)
+        b = prob.bias.float().numpy().astype(np.float64)[:, None] + np.zeros((70, 90))
+        assert np.array_equal(got, np.where(b > 0, b, 0.0))
+    elif variant == "gemm2":
+        p1 = workloads.make_problem(300, 264, 136, seed=149, kind="smallint", bias_mode="row")
+        p2 = workloads.make_problem(300, 264, 72, seed=150, kind="smallint", bias_mode=None)
+        C = ge.gemm2_epilogue(p1.A.cuda(), p1.B.cuda(), p2.A.cuda(), p2.B.cuda(), p1.bias.cuda(), **kw)
+        torch.cuda.synchronize()
+        out, _ = oracle.gemm2_epilogue(p1.A, p1.B, p2.A, p2.B, 300, 264, 136, 72, bias=p1.bias, act="relu")
+        assert np.array_equal(C.float().cpu().numpy().astype(np.float64), exact_expect(out, torch.float16))
+    else:
+        prob = _eighths_problem(300, 264, 96, seed=151)
+        got = run_gpu(prob, "rr", op="literal_bias_relu", **kw)
+        lit, _ = oracle_run(prob, "rr", literal_round=True)
+        assert np.array_equal(got, exact_expect(lit, torch.float16))
