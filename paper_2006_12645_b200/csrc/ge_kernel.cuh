@@ -72,6 +72,17 @@
 #ifndef GE_PAIR_ACQ
 #define GE_PAIR_ACQ 0
 #endif
+// Stage release group: the MMA warp commits once per GE_RELEASE_GROUP ring slots (2 = paired
+// release; 4 where the ring holds a multiple of 4 stages).
+#ifndef GE_RELEASE_GROUP
+#define GE_RELEASE_GROUP 2
+#endif
+// tcgen05.fence::after_thread_sync after every full-barrier wait of the MMA warp (1), or only after
+// the waits that order TMEM accesses (tile starts, accumulator-empty waits) (0): the TMA bytes a full
+// barrier announces are async-proxy writes the MMA (async proxy) may read once the phase completed.
+#ifndef GE_FENCE_FULL
+#define GE_FENCE_FULL 1
+#endif
 
 namespace ge {
 
@@ -146,7 +157,9 @@ enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY
              // of this CTA's epilogue, and its exit (after teardown)
              DBG_G_ENTRY = 16, DBG_G_START = 17, DBG_G_EPI_END = 18, DBG_G_EXIT = 19,
              // prologue transform warps: cycles blocked on a landed stage, cycles rewriting stages
-             DBG_XF_WAIT = 20, DBG_XF_WORK = 21, DBG_SLOTS = 22 };
+             DBG_XF_WAIT = 20, DBG_XF_WORK = 21,
+             // MMA warp (single-accumulator-half kernels): cycles issuing the k-block MMAs, cycles in commits
+             DBG_MMA_ISSUE = 22, DBG_MMA_COMMIT = 23, DBG_SLOTS = 24 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -339,6 +352,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     constexpr int NH = C_::kNHalves;
     constexpr int HALF_COLS = BN / NH;
     constexpr bool kPairAcq = GE_PAIR_ACQ && !PRO && NH == 1 && !MC && GE_PAIR_RELEASE;
+    constexpr int kRel = (GE_PAIR_RELEASE && !kPairAcq) ? ((GE_RELEASE_GROUP == 4 && S % 4 == 0) ? 4 : 2) : 1;
     const bool A_MN = p.a_mn != 0, B_MN = p.b_mn != 0;       // MN-major (row-major B / col-major A)
     const uint32_t IDESC = ptx::make_idesc_f16(C_::kRows * CG, C_::kUmmaN, A_MN, B_MN);
 
@@ -443,8 +457,11 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                     // paired release: the MMA warp commits only the odd stage of each pair (that
                     // commit covers the even stage's MMAs too), so wait once per pair on it
-                    if (!GE_PAIR_RELEASE) ptx::mbar_wait_timed(&empty_bar[s], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
-                    else if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                    if (kPairAcq) {
+                        if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                    } else if (s % kRel == 0) {
+                        ptx::mbar_wait_timed(&empty_bar[s + kRel - 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                    }
                     // paired acquire: both slots of a pair signal the even slot's full barrier, armed
                     // once for the pair's bytes; a piece with an odd k-block count ends on a single
                     // (the odd slot is skipped, MMA and producer agree on the rule)
@@ -558,7 +575,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 };
                 auto release_stage = [&](int stage) {
                     // MC: the stage's B halves came from both pairs, so both pairs' producers wait for it
-                    if (!GE_PAIR_RELEASE || (stage & 1)) ptx::mma_commit_elect<CG>(&empty_bar[stage], MC ? 0xF : 0x3);
+                    if (stage % kRel == kRel - 1) ptx::mma_commit_elect<CG>(&empty_bar[stage], MC ? 0xF : 0x3);
                 };
                 auto mma_half = [&](int stage, int kb, int h) {
                     ptx::mma_kblock<CG>(d_tmem + h * C_::kUmmaN, desc_a(stage), desc_b(stage, h), IDESC, kb != pc.kb0,
@@ -640,7 +657,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 } else {
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                         if (!(GE_EARLY_TEST && next_ready)) wait_ready(s, phase, dl[DBG_MMA_FULL]);
-                        ptx::tc_fence_after();
+                        if (GE_FENCE_FULL || PRO) ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             // first k-block of a tile: the epilogue must have drained this buffer
                             ptx::mbar_wait_timed(&tempty_bar[acc], acc_phase ^ 1,
@@ -653,9 +670,15 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             const int sn = s + 1 == S ? 0 : s + 1;
                             next_ready = ptx::mbar_test(PRO ? &xform_bar[sn] : &full_bar[sn], s + 1 == S ? phase ^ 1 : phase);
                         }
+                        const long long ti0 = dbg ? clock64() : 0;
                         mma_half(s, kb, 0);
+                        const long long ti1 = dbg ? clock64() : 0;
                         release_stage(s);                         // smem slot free once these MMAs finish
                         if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
+                        if (dbg && lane == 0) {
+                            dl[DBG_MMA_ISSUE] += static_cast<unsigned long long>(ti1 - ti0);
+                            dl[DBG_MMA_COMMIT] += static_cast<unsigned long long>(clock64() - ti1);
+                        }
                         if (++s == S) { s = 0; phase ^= 1; }
                     }
                 }
