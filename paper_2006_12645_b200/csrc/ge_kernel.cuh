@@ -72,6 +72,10 @@
 #ifndef GE_PAIR_ACQ
 #define GE_PAIR_ACQ 0
 #endif
+// Producer as a converged warp issuing TMA through elect.sync (1), or lane 0 alone (0).
+#ifndef GE_PROD_WARP
+#define GE_PROD_WARP 1
+#endif
 // Stage release group: the MMA warp commits once per GE_RELEASE_GROUP ring slots (2 = paired
 // release; 4 where the ring holds a multiple of 4 stages).
 #ifndef GE_RELEASE_GROUP
@@ -159,7 +163,9 @@ enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY
              // prologue transform warps: cycles blocked on a landed stage, cycles rewriting stages
              DBG_XF_WAIT = 20, DBG_XF_WORK = 21,
              // MMA warp (single-accumulator-half kernels): cycles issuing the k-block MMAs, cycles in commits
-             DBG_MMA_ISSUE = 22, DBG_MMA_COMMIT = 23, DBG_SLOTS = 24 };
+             DBG_MMA_ISSUE = 22, DBG_MMA_COMMIT = 23,
+             // TMA producer: cycles from a free slot to its loads issued, and the whole producer loop
+             DBG_PROD_ISSUE = 24, DBG_PROD_TOTAL = 25, DBG_SLOTS = 26 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -442,7 +448,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 
     if (warp == 0) {
         // ===================== TMA producer =====================
-        if (lane == 0) {
+        // GE_PROD_WARP: the whole warp runs the loop converged (warp-uniform state) and one elected
+        // lane issues each TMA / expect_tx; otherwise lane 0 alone.
+        if (GE_PROD_WARP || lane == 0) {
             int s = 0;
             uint32_t phase = 0;
             const uint64_t pol_a = ptx::l2_policy(p.hint_a);
@@ -458,9 +466,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     // paired release: the MMA warp commits only the odd stage of each pair (that
                     // commit covers the even stage's MMAs too), so wait once per pair on it
                     if (kPairAcq) {
-                        if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                        if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg && lane == 0, dl[DBG_PROD_EMPTY]);
                     } else if (s % kRel == 0) {
-                        ptx::mbar_wait_timed(&empty_bar[s + kRel - 1], phase ^ 1, dbg, dl[DBG_PROD_EMPTY]);
+                        ptx::mbar_wait_timed(&empty_bar[s + kRel - 1], phase ^ 1, dbg && lane == 0, dl[DBG_PROD_EMPTY]);
                     }
                     // paired acquire: both slots of a pair signal the even slot's full barrier, armed
                     // once for the pair's bytes; a piece with an odd k-block count ends on a single
@@ -469,6 +477,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     uint64_t* const fb = kPairAcq ? &full_bar[s & ~1] : &full_bar[s];
                     const bool arm = !kPairAcq || (s & 1) == 0;
                     const uint32_t n_sub = pair_two ? 2u : 1u;
+                    const long long tp0 = dbg ? clock64() : 0;
                     // sum of matmuls (Listing 4): k-blocks past A.B's come from P.Q, same accumulator
                     const bool second = kb >= p.num_k_blocks1;
                     const CUtensorMap* map_a = second ? &tmap_p : &tmap_a;
@@ -478,23 +487,32 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     uint8_t* sb = smem_b + s * C_::kBStage;
                     if (GE_DBG && p.dbg_noload && (wi != 0 || kb >= S)) {
                         // timing experiment (GE_DEBUG_NOLOAD): operands stay resident, results invalid
-                        if (CG == 1 || leader) ptx::mbar_arrive(&full_bar[s]);
+                        if ((CG == 1 || leader) && (!GE_PROD_WARP || lane == 0)) ptx::mbar_arrive(&full_bar[s]);
                         if (++s == S) { s = 0; phase ^= 1; }
                         continue;
                     }
+                    auto expect = [&](uint32_t bytes) {
+                        if (GE_PROD_WARP) ptx::mbar_arrive_expect_tx_elect(fb, bytes);
+                        else ptx::mbar_arrive_expect_tx(fb, bytes);
+                    };
                     if constexpr (CG == 2 && !PRO) {
                         // The peer's bytes can only land after the leader's barrier entered this
                         // phase (the peer first waits on its empty[s], released by the MMA that
                         // consumed the previous phase), so a transiently negative tx-count is safe.
-                        if (leader && arm) ptx::mbar_arrive_expect_tx(fb, 2 * n_sub * C_::kStageBytes);
+                        if (leader && arm) expect(2 * n_sub * C_::kStageBytes);
                     } else {
                         // single CTAs, and every CTA of a prologue pair: its own transform warps wait
                         // for its own stage
-                        if (arm) ptx::mbar_arrive_expect_tx(fb, n_sub * C_::kStageBytes);
+                        if (arm) expect(n_sub * C_::kStageBytes);
                     }
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol, int cb) {
-                        if constexpr (CG == 2 && !PRO) ptx::tma_load_3d_pair(dst, map, fb, c0, c1, cb, pol);
-                        else ptx::tma_load_3d(dst, map, fb, c0, c1, cb, pol);
+                        if (GE_PROD_WARP) {
+                            if constexpr (CG == 2 && !PRO) ptx::tma_load_3d_pair_elect(dst, map, fb, c0, c1, cb);
+                            else ptx::tma_load_3d_elect(dst, map, fb, c0, c1, cb);
+                        } else {
+                            if constexpr (CG == 2 && !PRO) ptx::tma_load_3d_pair(dst, map, fb, c0, c1, cb, pol);
+                            else ptx::tma_load_3d(dst, map, fb, c0, c1, cb, pol);
+                        }
                     };
                     // A, and the Hadamard tile S with A's box and swizzle (element-aligned with A in smem)
                     auto load_a = [&](uint8_t* dst, const CUtensorMap* map, int cb) {
@@ -515,12 +533,9 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             // this CTA's 64-row half `pair` of the block, to both pairs' CTAs of rank `rank`
                             // (an MN-major half is one 64-wide swizzle atom; the K-major map's box is 64 rows)
                             const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
-                            if (B_MN)
-                                ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], nh + pair * 64, k0, b,
-                                                         mask, pol_b);
-                            else
-                                ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], k0, nh + pair * 64, b,
-                                                         mask, pol_b);
+                            const int c0 = B_MN ? nh + pair * 64 : k0, c1 = B_MN ? k0 : nh + pair * 64;
+                            if (GE_PROD_WARP) ptx::tma_load_3d_pair_mc_elect(sbh + pair * 8192, map_b, &full_bar[s], c0, c1, b, mask);
+                            else ptx::tma_load_3d_pair_mc(sbh + pair * 8192, map_b, &full_bar[s], c0, c1, b, mask, pol_b);
                         } else if (B_MN) {
 #pragma unroll
                             for (int i = 0; i < C_::kBBlockRows / 64; ++i)
@@ -529,11 +544,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             load(sbh, map_b, k0, nh, pol_b, b);
                         }
                     }
+                    if (dbg && lane == 0) dl[DBG_PROD_ISSUE] += static_cast<unsigned long long>(clock64() - tp0);
                     if (kPairAcq && (s & 1) == 0 && !pair_two) ++s;   // single at the end of a piece
                     if (++s == S) { s = 0; phase ^= 1; }
                 }
             }
         }
+        if (dbg && lane == 0) dl[DBG_PROD_TOTAL] = static_cast<unsigned long long>(clock64() - t_start);
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA, one thread) =====================
         if (leader && nkb > 0) {

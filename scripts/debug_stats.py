@@ -29,6 +29,7 @@ for k in ("prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull
     print(f"  {k:18s} {avg(k, lead):12.0f} cyc  ({100*avg(k, lead)/tot:5.1f}% of total)")
 print("  prologue transform (sum over its 4 warps): wait for stage", avg("xf_wait", lead), " rewrite", avg("xf_work", lead))
 print("  MMA warp: issue", avg("mma_issue", lead), " commits", avg("mma_commit", lead))
+print("  producer: issue", avg("prod_issue", lead), " wait empty", avg("prod_wait_empty", lead), " loop total", avg("prod_total", lead))
 # split-K epilogue phases (per warp lane 0, summed over the CTA's epilogue warps)
 print("  split-K: sends (sum over warps)", avg("epi_tmem_ld", lead), " owner compute+store (sum over warps)", avg("epi_math", lead))
 print("  per-CTA mma_wait_full min/max:", min(r["mma_wait_full"] for r in lead), max(r["mma_wait_full"] for r in lead))
