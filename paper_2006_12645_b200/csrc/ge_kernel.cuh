@@ -76,6 +76,11 @@
 #ifndef GE_PROD_WARP
 #define GE_PROD_WARP 1
 #endif
+// Split producer: warp 0 issues the A (and S) loads and arms the full barrier, warp 3 issues the B
+// loads of the same stage in parallel (converged-warp producers only).
+#ifndef GE_PROD_SPLIT
+#define GE_PROD_SPLIT 0
+#endif
 // Stage release group: the MMA warp commits once per GE_RELEASE_GROUP ring slots (2 = paired
 // release; 4 where the ring holds a multiple of 4 stages).
 #ifndef GE_RELEASE_GROUP
@@ -446,7 +451,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     const int nkb = p.num_k_blocks;
     const WorkSeq work(p, cluster_id, num_clusters);
 
-    if (warp == 0) {
+    constexpr bool kSplitProd = GE_PROD_SPLIT && GE_PROD_WARP;
+    if (warp == 0 || (kSplitProd && warp == 3)) {
         // ===================== TMA producer =====================
         // GE_PROD_WARP: the whole warp runs the loop converged (warp-uniform state) and one elected
         // lane issues each TMA / expect_tx; otherwise lane 0 alone.
@@ -487,7 +493,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     uint8_t* sb = smem_b + s * C_::kBStage;
                     if (GE_DBG && p.dbg_noload && (wi != 0 || kb >= S)) {
                         // timing experiment (GE_DEBUG_NOLOAD): operands stay resident, results invalid
-                        if ((CG == 1 || leader) && (!GE_PROD_WARP || lane == 0)) ptx::mbar_arrive(&full_bar[s]);
+                        if ((CG == 1 || leader) && (!GE_PROD_WARP || lane == 0) && warp == 0) ptx::mbar_arrive(&full_bar[s]);
                         if (++s == S) { s = 0; phase ^= 1; }
                         continue;
                     }
@@ -495,15 +501,19 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (GE_PROD_WARP) ptx::mbar_arrive_expect_tx_elect(fb, bytes);
                         else ptx::mbar_arrive_expect_tx(fb, bytes);
                     };
+                    // split producer: warp 0 arms the barrier and loads A (and S), warp 3 loads B; bytes
+                    // landing before the arm only make the tx-count transiently negative (the phase
+                    // still needs warp 0's arrival)
+                    const bool do_a = !kSplitProd || warp == 0, do_b = !kSplitProd || warp == 3;
                     if constexpr (CG == 2 && !PRO) {
                         // The peer's bytes can only land after the leader's barrier entered this
                         // phase (the peer first waits on its empty[s], released by the MMA that
                         // consumed the previous phase), so a transiently negative tx-count is safe.
-                        if (leader && arm) expect(2 * n_sub * C_::kStageBytes);
+                        if (leader && arm && do_a) expect(2 * n_sub * C_::kStageBytes);
                     } else {
                         // single CTAs, and every CTA of a prologue pair: its own transform warps wait
                         // for its own stage
-                        if (arm) expect(n_sub * C_::kStageBytes);
+                        if (arm && do_a) expect(n_sub * C_::kStageBytes);
                     }
                     auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1, uint64_t pol, int cb) {
                         if (GE_PROD_WARP) {
@@ -523,10 +533,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             load(dst, map, k0, m0, pol_a, cb);
                         }
                     };
-                    load_a(sa, map_a, b);
-                    if constexpr (PRO == 2) load_a(smem_s + s * C_::kSStage, &tmap_p, p.s_batched ? b : 0);
+                    if (do_a) {
+                        load_a(sa, map_a, b);
+                        if constexpr (PRO == 2) load_a(smem_s + s * C_::kSStage, &tmap_p, p.s_batched ? b : 0);
+                    }
 #pragma unroll
-                    for (int h = 0; h < NH; ++h) {
+                    for (int h = 0; h < NH && do_b; ++h) {
                         uint8_t* sbh = sb + h * C_::kBBlockBytes;
                         const int nh = n0 + h * C_::kUmmaN;
                         if constexpr (MC) {
