@@ -234,9 +234,11 @@ const char* ge_last_error_detail(void);
  * split-K factor (split_k > 1: every tile is computed by a cluster of split_k CTAs, one K-slice
  * each, and the fp32 partials are reduce-scattered through distributed shared memory in fixed
  * order -- no workspace; only for few, long tiles) and the stream-K workspace bytes.  The plan is
- * the one a launch makes when given opt->workspace of at least *workspace_bytes (without one, a
- * launch re-plans with stream-K off).  The option checks of the launch entry points apply
- * (GE_ERR_INVALID_VALUE for invalid combinations).  Any output pointer may be NULL.
+ * the one a launch of the UNSWAPPED problem makes when given opt->workspace of at least
+ * *workspace_bytes (without one, a launch re-plans with stream-K off); ge_plan_ex below also
+ * reports multicast and the swap-AB decision (which depends on the op's bias).  The option checks
+ * of the launch entry points apply (GE_ERR_INVALID_VALUE for invalid combinations).  Any output
+ * pointer may be NULL.
  */
 ge_status ge_plan(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                   const ge_options* opt, int32_t num_sms,
@@ -251,9 +253,8 @@ typedef struct {
     int32_t split_k, multicast, swap_ab;
 } ge_plan_info;
 
-/* ge_plan with every planning decision, including multicast clusters and swap-AB (layouts and
- * options matter: swap-AB depends on the bias mode and prologue; pass op through opt->... as for a
- * launch; the op's bias flag is taken from `op`). */
+/* ge_plan with every planning decision a launch makes, including multicast clusters, half-row
+ * pairs and swap-AB (which depends on the op's bias flag and opt->bias_mode / prologue). */
 ge_status ge_plan_ex(int64_t batch, int64_t M, int64_t N, int64_t K, int32_t layoutA, int32_t layoutB,
                      int32_t op, const ge_options* opt, int32_t num_sms, ge_plan_info* out);
 

@@ -28,3 +28,7 @@ cap batched64x2048 2048 2048 2048 rr none 64
 timeout 1200 python scripts/paper_sweep.py --cpg 20 --out $O/paper_sweep_cpg20.json > $O/paper_sweep_cpg20.log 2>&1
 timeout 1200 python scripts/paper_sweep.py --cpg 1 --out $O/paper_sweep.json > $O/paper_sweep.log 2>&1
 ls -la $O
+for t in memcheck synccheck racecheck; do
+  echo "== $t" >> $O/compute_sanitizer.txt
+  timeout 1200 compute-sanitizer --tool $t --print-limit 10 python scripts/sanitize.py >> $O/compute_sanitizer.txt 2>&1
+done

@@ -1,7 +1,7 @@
 """Dev tool: GPU time per launch (CUDA-graph replay of 20 launches, operands L2-resident unless
 --cold) for a list of shapes with the library selected by GE_LIBRARY_FILE; leading dimensions
 padded to 8 elements like bench.py.
-usage: timed_multi.py "M N K lay [bn cg]" ... [--iters N] [--cold] [--alt LAY2] [--tile-m 128|256]
+usage: timed_multi.py "M N K lay [bn cg]" ... [--iters N] [--cold] [--alt LAY2] [--tile-m 128|256] [--prologue scale_k] [--kw "swap_ab=1,stream_k=1"]
 --alt LAY2: the graph alternates launches of layout `lay` and layout LAY2 (two kernel instantiations
 back to back, like bench.py's multi-layout steps)."""
 import os
@@ -12,7 +12,10 @@ import paper_2006_12645_b200 as ge
 
 alt = sys.argv[sys.argv.index("--alt") + 1] if "--alt" in sys.argv else None
 tm = int(sys.argv[sys.argv.index("--tile-m") + 1]) if "--tile-m" in sys.argv else 0
-args = [a for a in sys.argv[1:] if not a.startswith("--") and a != alt and a != str(tm)]
+pro = sys.argv[sys.argv.index("--prologue") + 1] if "--prologue" in sys.argv else None
+extra = sys.argv[sys.argv.index("--kw") + 1] if "--kw" in sys.argv else ""
+xkw = {k: int(v) for k, v in (x.split("=") for x in extra.split(",") if x)}
+args = [a for a in sys.argv[1:] if not a.startswith("--") and a not in (alt, str(tm), pro, extra)]
 iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 400
 if "--iters" in sys.argv:
     args.remove(str(iters))
@@ -41,14 +44,17 @@ for spec in args:
         nset *= 2
     bias = torch.randn(N, device="cuda", dtype=torch.float16)
     C = torch.empty(M, ld8(N), device="cuda", dtype=torch.float16)[:, :N]
+    scale = (torch.rand(K, device="cuda") + 0.5) if pro == "scale_k" else None
+    kw = dict(prologue=pro, scale=scale) if pro else {}
+    kw.update(xkw)
     G = 20
     for i in range(3):
-        ge.gemm_epilogue(As[i % nset], Bs[i % nset], bias, out=C, tile_n=bn, cta_group=cg, tile_m=tm)
+        ge.gemm_epilogue(As[i % nset], Bs[i % nset], bias, out=C, tile_n=bn, cta_group=cg, tile_m=tm, **kw)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for i in range(G):
-            ge.gemm_epilogue(As[i % nset], Bs[i % nset], bias, out=C, tile_n=bn, cta_group=cg, tile_m=tm)
+            ge.gemm_epilogue(As[i % nset], Bs[i % nset], bias, out=C, tile_n=bn, cta_group=cg, tile_m=tm, **kw)
     g.replay()
     torch.cuda.synchronize()
     reps = max(1, iters // G)
@@ -59,8 +65,10 @@ for spec in args:
     e.record()
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / (reps * G) * 1e-3
-    pl = ge.plan(M, N, K, layouts=lay, tile_n=bn, cta_group=cg, tile_m=tm)
+    pl = ge.plan(M, N, K, layouts=lay, tile_n=bn, cta_group=cg, tile_m=tm, prologue=pro, **xkw)
     if alt:
         spec = spec + "/" + alt
+    if extra:
+        spec = spec + " " + extra
     print(f"{lib:28s} {spec:26s} {t * 1e6:8.2f} us {2 * M * N * K / t / 1e12:7.1f} TF/s  "
           f"plan {pl['tile_m']}x{pl['tile_n']} cg{pl['cta_group']} split{pl['split_k']} swap{pl['swap_ab']}", flush=True)
