@@ -244,3 +244,36 @@ def test_binding_rejects_bad_tensors(ge):
 def test_tensor_map_cache_stats_exported(ge):
     s = ge.tensor_map_cache_stats()
     assert set(s) == {"hits", "misses"} and s["hits"] >= 0 and s["misses"] >= 0
+
+
+def test_validate_round2_options(lib, ge):
+    """Hadamard prologue tile, swap_ab and tile_m option checks (no device needed)."""
+    S = ge.Status
+    T = P * 256                                          # a fake, aligned prologue tile
+    assert v(lib, opt=opts(ge, prologue=3)) == S.INVALID_VALUE                          # no tile
+    assert v(lib, opt=opts(ge, prologue=3, prologue_tile=T)) == 0                       # packed ld
+    assert v(lib, opt=opts(ge, prologue=3, prologue_tile=T + 2)) == S.MISALIGNED
+    assert v(lib, opt=opts(ge, prologue=3, prologue_tile=T, ld_prologue_tile=60)) == S.INVALID_VALUE   # < K
+    assert v(lib, opt=opts(ge, prologue=3, prologue_tile=T, ld_prologue_tile=68)) == S.MISALIGNED      # 136 B rows
+    assert v(lib, opt=opts(ge, prologue=3, prologue_tile=T, ld_prologue_tile=72)) == 0
+    assert v(lib, la=1, opt=opts(ge, prologue=3, prologue_tile=T, ld_prologue_tile=64)) == S.INVALID_VALUE  # < M
+    assert v(lib, C=T, opt=opts(ge, prologue=3, prologue_tile=T)) == S.ALIASING        # C overlaps S
+    assert v(lib, opt=opts(ge, prologue=4)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, swap_ab=3)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, swap_ab=2)) == 0
+    assert v(lib, opt=opts(ge, tile_m=64)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, tile_m=256, cta_group=1)) == S.INVALID_VALUE
+    assert v(lib, opt=opts(ge, tile_m=128, cta_group=2, tile_n=512)) == S.INVALID_VALUE  # half-row: BN 128/256
+    assert v(lib, opt=opts(ge, tile_m=128, cta_group=2, tile_n=256)) == 0
+
+
+def test_plan_ex_round2_decisions(ge):
+    """ge_plan_ex reports half-row pairs, multicast and swap-AB as a launch would decide them."""
+    p = ge.plan(1024, 1024, 1024, tile_m=128, cta_group=2, tile_n=256)
+    assert (p["tile_m"], p["tile_n"], p["cta_group"], p["num_tiles"]) == (128, 256, 2, 8 * 4)
+    assert ge.plan(1024, 1024, 1024, tile_m=256)["tile_m"] in (256, 512)
+    assert ge.plan(35, 8457, 2560, op="relu")["swap_ab"] == 1                        # no bias: legal
+    p = ge.plan(4096, 4096, 4096, multicast=2, tile_n=256)
+    assert p["multicast"] == 1 and p["tile_m"] == 512
+    with pytest.raises(ge.GEError):
+        ge.plan(1024, 1024, 1024, tile_m=128, cta_group=2, tile_n=64)
