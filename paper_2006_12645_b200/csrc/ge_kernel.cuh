@@ -81,6 +81,11 @@
 #ifndef GE_PROD_SPLIT
 #define GE_PROD_SPLIT 0
 #endif
+// Early fill: single-CTA kernels issue their first ring pass of loads before the setup barrier
+// (measured slower on 1024^3 and the split-K shapes, profiles/r02_ab_early_fill.txt: off).
+#ifndef GE_EARLY_FILL
+#define GE_EARLY_FILL 0
+#endif
 // Stage release group: the MMA warp commits once per GE_RELEASE_GROUP ring slots (2 = paired
 // release; 4 where the ring holds a multiple of 4 stages).
 #ifndef GE_RELEASE_GROUP
@@ -410,65 +415,44 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         if (PRO == 2) ptx::tma_prefetch(&tmap_p);      // Hadamard S (the P slot: no sum of matmuls here)
         if (p.c_tma) ptx::tma_prefetch(&tmap_c);
     }
-    if (warp == 1 && lane == 0) {
-        for (int s = 0; s < S; ++s) {
-            // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier and
-            // only the leader's producer arrives (expecting both CTAs' bytes).
-            ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], MC ? 2 : 1);      // MC: both pairs' MMAs read stage s's B
-            ptx::mbar_init(&xform_bar[s], kXformWarps * CG);
-        }
-        for (int b = 0; b < 2; ++b) ptx::mbar_init(&tfull_bar[b], 1);
-        for (int b = 0; b < 4; ++b) ptx::mbar_init(&tempty_bar[b], EPI_WARPS * CG);
-        ptx::mbar_init(peer_ready_bar, split_cluster ? p.splits - 1 : 1);
-        ptx::mbar_init(recv_full_bar, 1);
-        ptx::fence_mbar_init();
-    }
-    if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
-    ptx::tc_fence_before();
-    if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
-    // prefetch, cluster sync) overlapped the previous kernel's tail; wait for it to complete before
-    // touching global memory, then let the next launch in the stream get scheduled.
-    ptx::grid_dependency_wait();
-    ptx::launch_dependents();
-
+    // Work sequence and diagnostics registers (independent of the setup barrier below).
+    const int cluster_id = blockIdx.x / CL;
+    const int num_clusters = gridDim.x / CL;
+    const int nkb = p.num_k_blocks;
+    const WorkSeq work(p, cluster_id, num_clusters);
     // Diagnostics accumulate in registers (a global read-modify-write per barrier wait would add
     // an L2 round trip to every pipeline step) and are flushed once per thread at teardown.
     const bool dbg = GE_DBG && p.dbg != nullptr;
     unsigned long long dl[DBG_SLOTS];
 #pragma unroll
     for (int i = 0; i < DBG_SLOTS; ++i) dl[i] = 0;
-    const long long t_start = clock64();
-    if (dbg && warp == 1 && lane == 0) {
-        dl[DBG_G_ENTRY] = g_entry;
-        dl[DBG_G_START] = globaltimer();
-    }
-    const int cluster_id = blockIdx.x / CL;
-    const int num_clusters = gridDim.x / CL;
-    const int nkb = p.num_k_blocks;
-    const WorkSeq work(p, cluster_id, num_clusters);
+    long long t_start = 0;
 
+    // ---- TMA producer loop, resumable (state kept across calls): `produce(n)` issues the loads of
+    // at most n more k-blocks of this CTA's work sequence, waiting for free ring slots as needed.
     constexpr bool kSplitProd = GE_PROD_SPLIT && GE_PROD_WARP;
-    if (warp == 0 || (kSplitProd && warp == 3)) {
-        // ===================== TMA producer =====================
-        // GE_PROD_WARP: the whole warp runs the loop converged (warp-uniform state) and one elected
-        // lane issues each TMA / expect_tx; otherwise lane 0 alone.
-        if (GE_PROD_WARP || lane == 0) {
-            int s = 0;
-            uint32_t phase = 0;
-            const uint64_t pol_a = ptx::l2_policy(p.hint_a);
-            const uint64_t pol_b = ptx::l2_policy(p.hint_b);
-            for (int wi = 0; wi < work.count(); ++wi) {
-                const Piece pc = work.get(wi);
-                const long long t = pc.tile;
-                int b, mt, nt;
-                decode_tile(p, t, TILE_M, b, mt, nt);
-                const int m0 = mt * TILE_M + pair * C_::kTileM + rank * C_::kRows;
-                const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
-                for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
+    int pr_wi = 0, pr_kb = 0, pr_s = 0;
+    uint32_t pr_phase = 0;
+    bool pr_open = false;
+    const uint64_t pol_a = ptx::l2_policy(p.hint_a);
+    const uint64_t pol_b = ptx::l2_policy(p.hint_b);
+    auto produce = [&](int budget) {
+        int& s = pr_s;
+        uint32_t& phase = pr_phase;
+        while (pr_wi < work.count() && budget > 0) {
+            const int wi = pr_wi;
+            const Piece pc = work.get(wi);
+            if (!pr_open) {
+                pr_kb = pc.kb0;
+                pr_open = true;
+            }
+            const long long t = pc.tile;
+            int b, mt, nt;
+            decode_tile(p, t, TILE_M, b, mt, nt);
+            const int m0 = mt * TILE_M + pair * C_::kTileM + rank * C_::kRows;
+            const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
+            for (; pr_kb < pc.kb1 && budget > 0; ++pr_kb, --budget) {
+                const int kb = pr_kb;
                     // paired release: the MMA warp commits only the odd stage of each pair (that
                     // commit covers the even stage's MMAs too), so wait once per pair on it
                     if (kPairAcq) {
@@ -559,9 +543,59 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     if (dbg && lane == 0) dl[DBG_PROD_ISSUE] += static_cast<unsigned long long>(clock64() - tp0);
                     if (kPairAcq && (s & 1) == 0 && !pair_two) ++s;   // single at the end of a piece
                     if (++s == S) { s = 0; phase ^= 1; }
-                }
+            }
+            if (pr_kb >= pc.kb1) {
+                ++pr_wi;
+                pr_open = false;
             }
         }
+    };
+    // Early fill (single-CTA tiles): warp 0 initialises the barriers and issues the first ring pass
+    // of loads right away, so their latency overlaps the TMEM allocation and the setup barrier (the
+    // TMA touches only this CTA's barriers; pairs and multicast clusters signal peer barriers and
+    // must wait for the cluster barrier).
+    constexpr bool kEarly = GE_EARLY_FILL && CG == 1 && !MC && !kSplitProd;
+    if (warp == (kEarly ? 0 : 1) && lane == 0) {
+        for (int s = 0; s < S; ++s) {
+            // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier and
+            // only the leader's producer arrives (expecting both CTAs' bytes).
+            ptx::mbar_init(&full_bar[s], 1);
+            ptx::mbar_init(&empty_bar[s], MC ? 2 : 1);      // MC: both pairs' MMAs read stage s's B
+            ptx::mbar_init(&xform_bar[s], kXformWarps * CG);
+        }
+        for (int b = 0; b < 2; ++b) ptx::mbar_init(&tfull_bar[b], 1);
+        for (int b = 0; b < 4; ++b) ptx::mbar_init(&tempty_bar[b], EPI_WARPS * CG);
+        ptx::mbar_init(peer_ready_bar, split_cluster ? p.splits - 1 : 1);
+        ptx::mbar_init(recv_full_bar, 1);
+        ptx::fence_mbar_init();
+    }
+    if (kEarly && warp == 0) {
+        __syncwarp();
+        ptx::grid_dependency_wait();                 // inputs may come from the previous kernel
+        if (GE_PROD_WARP || lane == 0) produce(S);
+    }
+    if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
+    ptx::tc_fence_before();
+    if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
+    // prefetch, cluster sync) overlapped the previous kernel's tail; wait for it to complete before
+    // touching global memory, then let the next launch in the stream get scheduled.
+    ptx::grid_dependency_wait();
+    ptx::launch_dependents();
+
+    t_start = clock64();
+    if (dbg && warp == 1 && lane == 0) {
+        dl[DBG_G_ENTRY] = g_entry;
+        dl[DBG_G_START] = globaltimer();
+    }
+    if (warp == 0 || (kSplitProd && warp == 3)) {
+        // ===================== TMA producer =====================
+        // GE_PROD_WARP: the whole warp runs the loop converged (warp-uniform state) and one elected
+        // lane issues each TMA / expect_tx; otherwise lane 0 alone.  With the early fill the first
+        // ring pass was issued before the setup barrier; this continues where it stopped.
+        if (GE_PROD_WARP || lane == 0) produce(0x7fffffff);
         if (dbg && lane == 0) dl[DBG_PROD_TOTAL] = static_cast<unsigned long long>(clock64() - t_start);
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA, one thread) =====================
