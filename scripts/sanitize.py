@@ -28,7 +28,7 @@ for (M, N, K) in [(300, 520, 200), (129, 257, 65)]:
     ge.gemm_epilogue(A, B, bias, prologue="hadamard", scale=S, stream_k=1)
     ge.gemm_epilogue(A, B, bias, prologue="hadamard", scale=S, tile_n=512, cta_group=2)
     ge.gemm_epilogue(A[:35], B, bias, swap_ab=2)
-    ge.gemm_epilogue(A.t().contiguous().t(), B.t().contiguous(), bias, tile_n=256, cta_group=2)   # cr
+    ge.gemm_epilogue(A.t().contiguous().t(), B.contiguous(), bias, tile_n=256, cta_group=2)   # cr
     # split-K clusters (DSMEM reduce-scatter): a long-K shape the planner splits
     A2 = torch.randn(256, 64 * 40, device="cuda", dtype=torch.float16)
     B2 = torch.randn(64 * 40, 256, device="cuda", dtype=torch.float16)
