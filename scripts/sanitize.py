@@ -21,14 +21,18 @@ for (M, N, K) in [(300, 520, 200), (129, 257, 65)]:
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=2, multicast=2)
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=2, multicast=2, out_dtype=torch.float32)
     # round 2: half-row CTA pairs, swap-AB (skinny, transposed store), Hadamard prologue, all layouts
-    S = torch.rand(M, up8(K), device="cuda").half()[:, :K] + 0.5
+    S = (torch.rand(M, up8(K), device="cuda") + 0.5).half()[:, :K]
     for bn in (128, 256):
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=2, tile_m=128)
         ge.gemm_epilogue(A, B, bias, tile_n=bn, cta_group=2, tile_m=128, out_dtype=torch.float32)
     ge.gemm_epilogue(A, B, bias, prologue="hadamard", scale=S, stream_k=1)
     ge.gemm_epilogue(A, B, bias, prologue="hadamard", scale=S, tile_n=512, cta_group=2)
     ge.gemm_epilogue(A[:35], B, bias, swap_ab=2)
-    ge.gemm_epilogue(A.t().contiguous().t(), B.contiguous(), bias, tile_n=256, cta_group=2)   # cr
+    Acr = torch.empty(K, up8(M), device="cuda", dtype=torch.float16)[:, :M]       # column-major A, padded ld
+    Acr.copy_(A.t())
+    Brr = torch.empty(K, up8(N), device="cuda", dtype=torch.float16)[:, :N]       # row-major B, padded ld
+    Brr.copy_(B)
+    ge.gemm_epilogue(Acr.t(), Brr, bias, tile_n=256, cta_group=2)                  # cr, runtime layouts
     # split-K clusters (DSMEM reduce-scatter): a long-K shape the planner splits
     A2 = torch.randn(256, 64 * 40, device="cuda", dtype=torch.float16)
     B2 = torch.randn(64 * 40, 256, device="cuda", dtype=torch.float16)
