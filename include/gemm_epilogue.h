@@ -268,13 +268,13 @@ void ge_tensor_map_cache_stats(uint64_t* hits, uint64_t* misses);
 
 /*
  * Diagnostics: when the process runs with GE_DEBUG_STATS=1 (diagnostics build), every launch
- * records per-CTA counters (26 x uint64 per CTA: total cycles, producer cycles blocked on free
+ * records per-CTA counters (30 x uint64 per CTA: total cycles, producer cycles blocked on free
  * stages, MMA cycles blocked on loaded stages, MMA cycles blocked on a drained accumulator,
  * epilogue cycles blocked on a full accumulator, epilogue phase timings, and %globaltimer
  * stamps (ns) of kernel entry, end of setup, end of the epilogue and exit, then the prologue
  * transform warps' cycles blocked on landed stages and spent rewriting them, and the MMA warp's
  * cycles issuing k-block MMAs and committing, the TMA producer's cycles issuing loads and its loop
- * total).  Copies the last launch's counters of up to
+ * total, and the split-K owner's TMEM-load / partial-add / math / store cycles).  Copies the last launch's counters of up to
  * max_ctas CTAs into out (synchronizing) and returns how many were copied (0 when disabled).
  */
 int32_t ge_debug_read(uint64_t* out, int32_t max_ctas);

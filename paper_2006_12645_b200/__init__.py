@@ -497,13 +497,14 @@ def debug_stats(max_ctas: int = 148):
     """Per-CTA blocked-cycle counters of the last launch (needs GE_DEBUG_STATS=1), as a list of
     dicts, or [] when diagnostics are off.  Synchronizes."""
     import numpy as np
-    buf = np.zeros((max_ctas, 26), dtype=np.uint64)
+    buf = np.zeros((max_ctas, 30), dtype=np.uint64)
     n = load_library().ge_debug_read(buf.ctypes.data, max_ctas)
     keys = ("total", "prod_wait_empty", "mma_wait_full", "mma_wait_tempty", "epi_wait_tfull", "epi_to_release0",
             "epi_to_release1", "epi_tile", "epi_tmem_ld", "epi_math", "sk_owner_wait", "sk_partial_write",
             "sk_pieces", "epi_end", "reserved", "first_mma", "g_entry", "g_start", "g_epi_end", "g_exit",
-            "xf_wait", "xf_work", "mma_issue", "mma_commit", "prod_issue", "prod_total")
-    return [dict(zip(keys, (int(x) for x in buf[i, :26]))) for i in range(n)]
+            "xf_wait", "xf_work", "mma_issue", "mma_commit", "prod_issue", "prod_total",
+            "own_ld", "own_add", "own_math", "own_st")
+    return [dict(zip(keys, (int(x) for x in buf[i, :30]))) for i in range(n)]
 
 
 def version() -> str:

@@ -175,7 +175,9 @@ enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY
              // MMA warp (single-accumulator-half kernels): cycles issuing the k-block MMAs, cycles in commits
              DBG_MMA_ISSUE = 22, DBG_MMA_COMMIT = 23,
              // TMA producer: cycles from a free slot to its loads issued, and the whole producer loop
-             DBG_PROD_ISSUE = 24, DBG_PROD_TOTAL = 25, DBG_SLOTS = 26 };
+             DBG_PROD_ISSUE = 24, DBG_PROD_TOTAL = 25,
+             // split-K owner phases (summed over warps): TMEM load, partial adds, math, stores
+             DBG_OWN_LD = 26, DBG_OWN_ADD = 27, DBG_OWN_MATH = 28, DBG_OWN_ST = 29, DBG_SLOTS = 30 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -1093,9 +1095,11 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     for (int j = 0; j < CPH; ++j) {
                         const int c = j * NG + grp;
                         if (owner(c) != js) continue;
+                        const long long tq0 = dbg ? clock64() : 0;
                         uint32_t v[W];
                         load(c, v);
                         ptx::tmem_ld_wait_regs(v);
+                        const long long tq1 = dbg ? clock64() : 0;
                         const uint8_t* rb = smem_a + (4 * c + q - u_lo(js)) * (S - 1) * UB + lane * 16;
 #pragma unroll 1
                         for (int s2 = 0; s2 < S - 1; ++s2) {
@@ -1108,9 +1112,17 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                                 v[4 * g + 3] = __float_as_uint(__uint_as_float(v[4 * g + 3]) + pv.w);
                             }
                         }
+                        const long long tq2 = dbg ? clock64() : 0;
                         uint32_t w[NWORD];
                         compute(c, v, w);
+                        const long long tq3 = dbg ? clock64() : 0;
                         store(c, w);
+                        if (dbg && lane == 0) {
+                            dl[DBG_OWN_LD] += static_cast<unsigned long long>(tq1 - tq0);
+                            dl[DBG_OWN_ADD] += static_cast<unsigned long long>(tq2 - tq1);
+                            dl[DBG_OWN_MATH] += static_cast<unsigned long long>(tq3 - tq2);
+                            dl[DBG_OWN_ST] += static_cast<unsigned long long>(clock64() - tq3);
+                        }
                     }
                     if (dbg && lane == 0) dl[DBG_EPI_MATH] += static_cast<unsigned long long>(clock64() - to0);   // owner
                     release(0);

@@ -31,6 +31,8 @@ print("  prologue transform (sum over its 4 warps): wait for stage", avg("xf_wai
 print("  MMA warp: issue", avg("mma_issue", lead), " commits", avg("mma_commit", lead))
 print("  producer: issue", avg("prod_issue", lead), " wait empty", avg("prod_wait_empty", lead), " loop total", avg("prod_total", lead))
 # split-K epilogue phases (per warp lane 0, summed over the CTA's epilogue warps)
+print("  split-K owner phases (sum over warps): tmem ld", avg("own_ld", lead), " add", avg("own_add", lead),
+      " math", avg("own_math", lead), " store", avg("own_st", lead))
 print("  split-K: sends (sum over warps)", avg("epi_tmem_ld", lead), " owner compute+store (sum over warps)", avg("epi_math", lead))
 print("  per-CTA mma_wait_full min/max:", min(r["mma_wait_full"] for r in lead), max(r["mma_wait_full"] for r in lead))
 
