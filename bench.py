@@ -358,6 +358,7 @@ def time_steps(w, steps, warmup, stream, torch, dist, world, graph=True, clock=N
     n0 = w.ge.launch_count()
     ctx = clock if clock is not None else _NullCtx()
     with ctx:
+        gpu_busy(torch, stream)
         t0.record(stream)
         if g_timed is not None:
             g_timed.replay()
@@ -376,6 +377,14 @@ def time_steps(w, steps, warmup, stream, torch, dist, world, graph=True, clock=N
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     return ms, kern_ms, n_launch
+
+
+def gpu_busy(torch, stream):
+    """Queue ~1 ms of device spin ahead of the start event: the host-side submission of the timed
+    graph (or of the first eager launches) then overlaps it, so the CUDA-event region holds only the
+    kernels being timed back to back, not the host's launch latency.  The spin runs before t0."""
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(2_000_000)
 
 
 class _NullCtx:
@@ -607,6 +616,7 @@ def compare_torch(torch, w, stream, iters=10):
         gr.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gpu_busy(torch, stream)
         e0.record(stream)
         gr.replay()
         e1.record(stream)

@@ -732,11 +732,18 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
         else ok = encode3d(&maps.q, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a.Q, a.N, a.K2, 1, a.ldq, 0, 64, 64);
         if (!ok) return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for Q");
     }
-    const bool c_tma = !c_trans && (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && ((a.ldc * es) % 16 == 0) &&
-                       (a.batch == 1 || (a.sC * es) % 16 == 0);
+    // swap-AB (c_trans): the map describes the caller's C (a.N rows of a.M columns); the kernel
+    // stages each 32 x 32 block transposed and stores it with the coordinates swapped.  The TMA store
+    // clips the inner dimension only at 16-B granularity (measured: a ragged width wrote into the
+    // caller's padding), so the map's inner extent is the width rounded down to 16 B and the kernel
+    // writes the ragged edge element-wise.
+    const int64_t c_inner = c_trans ? a.M : a.N, c_outer = c_trans ? a.N : a.M;
+    const int64_t c_ext = c_inner / (16 / es) * (16 / es);
+    const bool c_tma = (reinterpret_cast<uintptr_t>(a.C) % 16 == 0) && ((a.ldc * es) % 16 == 0) &&
+                       (a.batch == 1 || (a.sC * es) % 16 == 0) && c_ext > 0;
     if (c_tma) {
-        if (!encode3d(&maps.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, es, a.C, a.N,
-                      a.M, a.batch, a.ldc, a.sC, 32, 32, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+        if (!encode3d(&maps.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, es, a.C, c_ext,
+                      c_outer, a.batch, a.ldc, a.sC, 32, 32, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
             return fail(GE_ERR_CUDA, "cuTensorMapEncodeTiled failed for C");
     }
 
@@ -784,6 +791,7 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
     p.c_tma = c_tma ? 1 : 0;
     p.c_vec = c_tma ? 1 : 0;                      // same alignment conditions as the TMA store
     p.c_trans = c_trans ? 1 : 0;
+    p.c_ext = static_cast<int>(c_ext);
 
 #if GE_DBG
     // diagnostics build only (libgemm_epilogue_dbg.so): counters and timing experiments

@@ -142,6 +142,8 @@ struct Params {
     int c_vec;                      // st.global path may use 16-B vector stores (aligned rows)
     int c_trans;                    // swap-AB launch: the kernel computes
                                     // C^T = B^T A^T, so element (row, col) goes to C[col * ldc + row]
+    int c_ext;                      // TMA store: inner extent of the C map (C's width rounded down to
+                                    // 16 B; kernel columns, or kernel rows with c_trans)
     // L2 eviction priority of the operand loads / output stores (0 normal, 1 first, 2 last)
     int hint_a, hint_b, hint_c;
     // stream-K: tiles [dp_tiles, num_tiles) are split into sk_units
@@ -974,6 +976,29 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     }
                 }
             };
+            // element-wise st.global of this thread's row of chunk c: columns [lo, N) of it (normal), or,
+            // swap-AB, the thread's row is a column of C and the 32 lanes of the warp hold 32 consecutive
+            // C columns, so each store instruction writes one contiguous 64-B / 128-B segment of a C row
+            auto store_scalar = [&](const int col0, const uint32_t* w, const int lo) {
+                if (p.c_trans) {
+                    const long long cb = static_cast<long long>(b) * p.stride_c + row;
+#pragma unroll
+                    for (int e = 0; e < W; ++e) {
+                        if (col0 + e >= p.N) continue;
+                        const long long o = cb + static_cast<long long>(col0 + e) * p.ldc;
+                        if constexpr (OUT_F32) reinterpret_cast<float*>(p.C)[o] = __uint_as_float(w[e]);
+                        else reinterpret_cast<__half*>(p.C)[o] = reinterpret_cast<const __half*>(w)[e];
+                    }
+                } else {
+                    const long long off = static_cast<long long>(b) * p.stride_c + static_cast<long long>(row) * p.ldc;
+#pragma unroll
+                    for (int e = 0; e < W; ++e) {
+                        if (col0 + e < lo || col0 + e >= p.N) continue;
+                        if constexpr (OUT_F32) reinterpret_cast<float*>(p.C)[off + col0 + e] = __uint_as_float(w[e]);
+                        else reinterpret_cast<__half*>(p.C)[off + col0 + e] = reinterpret_cast<const __half*>(w)[e];
+                    }
+                }
+            };
             // packed row of chunk c -> C (TMA store through a swizzled staging chunk, or st.global)
             auto store = [&](const int ct, const uint32_t* w) {
                 const int col0 = nt * BN + (ct + qc) * W;
@@ -984,56 +1009,56 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                     if (lane == 0) ptx::bulk_wait_read<NBUF - 1>(); // the store that last used `buf` has read it
                     __syncwarp();
                     uint8_t* sc = stage_c + buf * STG;
+                    if (p.c_trans) {
+                        // swap-AB: the warp's 32 x 32 block of C^T is a 32 x 32 block of C (rows col0..,
+                        // columns row0..): staged transposed (smem row e = C row col0 + e, this lane's
+                        // element at column lane), one 64-B / 128-B row segment per element index, then
+                        // one TMA store into C's own tensor map (rows / columns past C clipped)
 #pragma unroll
-                    for (int g = 0; g < NV; ++g) {
-                        const int pc = (ROWB == 128) ? (g ^ (lane & 7)) : (g ^ ((lane >> 1) & 3));
-                        *reinterpret_cast<uint4*>(sc + lane * ROWB + pc * 16) =
-                            make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
+                        for (int e = 0; e < W; ++e) {
+                            if constexpr (OUT_F32) {
+                                const int pc = (lane >> 2) ^ (e & 7);
+                                *reinterpret_cast<uint32_t*>(sc + e * ROWB + pc * 16 + (lane & 3) * 4) = w[e];
+                            } else {
+                                const int pc = (lane >> 3) ^ ((e >> 1) & 3);
+                                *reinterpret_cast<uint16_t*>(sc + e * ROWB + pc * 16 + (lane & 7) * 2) =
+                                    static_cast<uint16_t>((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xFFFFu));
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int g = 0; g < NV; ++g) {
+                            const int pc = (ROWB == 128) ? (g ^ (lane & 7)) : (g ^ ((lane >> 1) & 3));
+                            *reinterpret_cast<uint4*>(sc + lane * ROWB + pc * 16) =
+                                make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
+                        }
                     }
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        ptx::tma_store_3d(&tmap_c, sc, col0, row0, b, pol_c);
+                        if (p.c_trans) ptx::tma_store_3d(&tmap_c, sc, row0, col0, b, pol_c);
+                        else ptx::tma_store_3d(&tmap_c, sc, col0, row0, b, pol_c);
                         ptx::bulk_commit();
                     }
                     buf = (buf + 1 == NBUF) ? 0 : buf + 1;
+                    // The TMA store clips the inner dimension at 16-B granularity, so the map's inner
+                    // extent is C's width rounded down to 16 B (c_ext) and the < 16 B ragged edge
+                    // [c_ext, width) goes out element-wise (the caller's padding past C stays untouched)
+                    if (p.c_trans) {
+                        if (row >= p.c_ext && row < p.M) store_scalar(col0, w, 0);
+                    } else if (col0 + W > p.c_ext && row < p.M) {
+                        store_scalar(col0, w, p.c_ext);
+                    }
                 } else if (row < p.M) {
                     // st.global path: C whose base/ldc breaks the TMA alignment rules (scalar stores),
                     // or 16-B aligned rows written straight from registers (c_vec)
-                    const long long off = static_cast<long long>(b) * p.stride_c + static_cast<long long>(row) * p.ldc;
-                    if (p.c_trans) {
-                        // swap-AB: this thread's row is a column of C; the 32 lanes of the warp hold
-                        // 32 consecutive C columns, so each store instruction writes one contiguous
-                        // 64-B (fp16) / 128-B (fp32) segment of a C row
-                        const long long cb = static_cast<long long>(b) * p.stride_c + row;
-                        if constexpr (OUT_F32) {
-#pragma unroll
-                            for (int e = 0; e < W; ++e)
-                                if (col0 + e < p.N)
-                                    reinterpret_cast<float*>(p.C)[cb + static_cast<long long>(col0 + e) * p.ldc] =
-                                        __uint_as_float(w[e]);
-                        } else {
-                            const __half* hv = reinterpret_cast<const __half*>(w);
-#pragma unroll
-                            for (int e = 0; e < W; ++e)
-                                if (col0 + e < p.N)
-                                    reinterpret_cast<__half*>(p.C)[cb + static_cast<long long>(col0 + e) * p.ldc] = hv[e];
-                        }
-                    } else if (p.c_vec && col0 + W <= p.N) {
+                    if (!p.c_trans && p.c_vec && col0 + W <= p.N) {
+                        const long long off = static_cast<long long>(b) * p.stride_c + static_cast<long long>(row) * p.ldc;
                         uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.C) + (off + col0) * ES);
 #pragma unroll
                         for (int g = 0; g < NV; ++g) dst[g] = make_uint4(w[4 * g], w[4 * g + 1], w[4 * g + 2], w[4 * g + 3]);
-                    } else if constexpr (OUT_F32) {
-                        float* crow = reinterpret_cast<float*>(p.C) + off;
-#pragma unroll
-                        for (int e = 0; e < W; ++e)
-                            if (col0 + e < p.N) crow[col0 + e] = __uint_as_float(w[e]);
                     } else {
-                        __half* crow = reinterpret_cast<__half*>(p.C) + off;
-                        const __half* hv = reinterpret_cast<const __half*>(w);
-#pragma unroll
-                        for (int e = 0; e < W; ++e)
-                            if (col0 + e < p.N) crow[col0 + e] = hv[e];
+                        store_scalar(col0, w, 0);
                     }
                 }
             };

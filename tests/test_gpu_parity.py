@@ -230,6 +230,30 @@ def test_padding_untouched():
     assert (Cbuf[:, 200:] == -5.0).all()
 
 
+@pytest.mark.parametrize("out_dtype", [torch.float16, torch.float32])
+@pytest.mark.parametrize("M,N,swap", [(64, 1030, 1), (300, 1027, 1), (35, 1030, 2), (35, 1027, 2), (300, 701, 1)])
+def test_padding_untouched_ragged_width(M, N, swap, out_dtype):
+    """A C width that is not a multiple of 16 B with a padded ldc (16-B aligned rows, so the TMA store
+    path): the TMA store clips its inner dimension only at 16-B granularity, so the library maps C's
+    width rounded down and writes the ragged edge element-wise; the padding past column N keeps its
+    contents and every element of C is right (bitwise, small integers), swapped and unswapped, batched."""
+    batch, K = 2, 136
+    probs = [workloads.make_problem(M, N, K, seed=150 + b, kind="smallint", bias_mode="row") for b in range(batch)]
+    A = torch.stack([p.A for p in probs]).cuda()
+    ldb = (N + 7) // 8 * 8
+    Bpad = torch.zeros((batch, K, ldb), dtype=torch.float16)
+    Bpad[:, :, :N] = torch.stack([p.B for p in probs])
+    B = Bpad.cuda()[:, :, :N]
+    bias = torch.stack([p.bias for p in probs]).cuda()
+    Cbuf = torch.full((batch, M, 1040), -5.0, dtype=out_dtype, device="cuda")
+    ge.gemm_epilogue_batched(A, B, bias, out=Cbuf[:, :, :N], swap_ab=swap)
+    torch.cuda.synchronize()
+    assert (Cbuf[:, :, N:] == -5.0).all()
+    for b, p in enumerate(probs):
+        out, _ = oracle_run(p, "rr")
+        assert np.array_equal(Cbuf[b, :, :N].float().cpu().numpy().astype(np.float64), exact_expect(out, out_dtype))
+
+
 @pytest.mark.parametrize("shared_bias", [True, False])
 def test_batched_matches_single(shared_bias):
     """Item b of the batched call equals the single call on item b, bitwise (DESIGN.md R-C14)."""
@@ -731,9 +755,11 @@ def test_hadamard_batched_and_host():
                                                    ("row", "literal_bias_relu", torch.float16)])
 def test_swap_ab_exact_and_bound(layouts, bias_mode, op, out_dtype):
     """C^T = B^T A^T with a transposed store: forced on a ragged problem (M = 37 rows of C become the
-    MMA's N, N = 1000 its 128-row side) and on a tile-exact one; ROW and COL bias trade places.
-    Small integers bitwise, uniform data within the bound (sigmoid: bound only)."""
-    for M, N, K in ((37, 1000, 200), (64, 256, 128)):
+    MMA's N, N = 1000 its 128-row side), on a tile-exact one, on C rows that break the TMA alignment
+    (N = 1001: the st.global transposed store) and on a long-K one (split-K clusters under the
+    transposed TMA store); ROW and COL bias trade places.  Small integers bitwise, uniform data within
+    the bound (sigmoid: bound only)."""
+    for M, N, K in ((37, 1000, 200), (64, 256, 128), (37, 1001, 200), (40, 2000, 1024)):
         for kind in ("smallint", "uniform"):
             prob = workloads.make_problem(M, N, K, seed=120, kind=kind, bias_mode=bias_mode or "none")
             assert ge.plan(M, N, K, layouts=layouts, swap_ab=2, bias_mode=bias_mode or "row")["swap_ab"] == 1
