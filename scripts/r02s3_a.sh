@@ -1,6 +1,6 @@
 #!/bin/bash
 # Re-entry check on the restored build: GPU tests, default bench line, split-K owner phase counters.
-O=gpurun_out/r03a
+O=gpurun_out/r02s3a
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err

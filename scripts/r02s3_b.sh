@@ -1,6 +1,6 @@
 #!/bin/bash
 # swap-AB transposed TMA store: parity, then bench + debug counters of the skinny shape
-O=gpurun_out/r03b
+O=gpurun_out/r02s3b
 mkdir -p $O
 timeout 600 python -m pytest tests -m gpu -q -x -k "swap or deepbench or smoke or padding or fallback or ragged or split" > $O/pytest_swap.log 2>&1; echo "rc=$?" >> $O/pytest_swap.log
 timeout 300 python bench.py --workload deepbench_b --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_deepbench_b.json 2> $O/bench.err

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B: skinny shapes, old (st.global transposed store) vs new (transposed TMA store); split-K vs none
-O=gpurun_out/r03c
+O=gpurun_out/r02s3c
 mkdir -p $O
 for rep in 1 2; do
 for v in old default; do
