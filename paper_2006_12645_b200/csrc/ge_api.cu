@@ -509,6 +509,10 @@ int group_m_for(const Plan& pl, const Args& a, int sms) {
     return 16;
 }
 
+// Diagnostics timeline (debug build, ge_debug_set_timeline): a caller-owned device buffer that
+// launches append %globaltimer stamps of CTA 0 to (no per-launch reset, so graph-replayed
+// back-to-back launches keep their programmatic-dependent-launch overlap).
+unsigned long long* g_timeline = nullptr;
 // Diagnostics (env GE_DEBUG_STATS=1, debug build): a zeroed per-CTA counter buffer per device.
 unsigned long long* g_dbg[64] = {};
 int g_dbg_ctas[64] = {};
@@ -796,6 +800,7 @@ ge_status launch_impl(Args& a, cudaStream_t st, bool c_trans) {
 #if GE_DBG
     // diagnostics build only (libgemm_epilogue_dbg.so): counters and timing experiments
     p.dbg = debug_buffer(sms);
+    p.tl = g_timeline;
     static const int noload = getenv("GE_DEBUG_NOLOAD") ? 1 : 0;   // timing experiment only
     p.dbg_noload = noload;
     static const int dflags = getenv("GE_DEBUG_FLAGS") ? atoi(getenv("GE_DEBUG_FLAGS")) : 0;   // experiments only
@@ -1224,6 +1229,10 @@ int32_t ge_debug_read(uint64_t* out, int32_t max_ctas) {
     }
     return n;
 }
+
+// Debug build only (not in the header): set the timeline buffer (nullptr: off).  Layout: word 0 =
+// launch counter, then 16 words per launch (see ge_kernel.cuh TL_*).
+void ge_debug_set_timeline(unsigned long long* dev_buf) { g_timeline = dev_buf; }
 
 const char* ge_version(void) { return "gemm_epilogue-b200 0.1.0 (sm_100a, tcgen05/TMA/TMEM)"; }
 

@@ -162,7 +162,15 @@ struct Params {
     // compile these branches out, so no environment variable can change their results)
     int dbg_noload;                 // GE_DEBUG_NOLOAD: stop issuing TMA after the ring is full once
     int dbg_flags;                  // GE_DEBUG_FLAGS: 1 skip epilogue, 8 no epilogue math, 16 no stores
+    unsigned long long* tl;         // timeline of CTA 0 (ge_debug_set_timeline), or nullptr
 };
+
+// Timeline stamps (%globaltimer ns) of CTA 0 per launch (diagnostics build): word 0 of the buffer
+// counts launches, launch i writes words 1 + 16 i + TL_*.
+enum : int { TL_ENTRY = 0, TL_SETUP = 1, TL_WAIT = 2, TL_FIRST_FULL = 3, TL_LAST_COMMIT = 4, TL_EPI_TFULL = 5,
+             TL_EPI_END = 6, TL_TEARDOWN = 7, TL_EXIT = 8, TL_PROD_FIRST = 9, TL_PROD_LAST = 10,
+             // producer's first k-block: tile decoded, empty slot acquired, expect_tx armed, A loads issued
+             TL_P_DECODE = 11, TL_P_EMPTY = 12, TL_P_EXPECT = 13, TL_P_LOADA = 14, TL_N = 16 };
 
 // Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
 enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
@@ -233,6 +241,26 @@ struct Cfg {
 };
 
 __device__ __forceinline__ void decode_tile(const Params& p, long long t, int tile_m, int& b, int& mt, int& nt) {
+    (void)tile_m;
+    if (p.num_tiles <= 0x7fffffffll) {
+        // 32-bit unsigned divisions (a 64-bit division is a long subroutine on the GPU and the
+        // producer's first decode sits right after griddepcontrol.wait)
+        const uint32_t ut = static_cast<uint32_t>(t);
+        const uint32_t per_batch = static_cast<uint32_t>(p.num_m_tiles) * static_cast<uint32_t>(p.num_n_tiles);
+        const uint32_t ub = ut / per_batch;
+        const uint32_t r = ut - ub * per_batch;
+        const uint32_t per_group = static_cast<uint32_t>(p.group_m) * static_cast<uint32_t>(p.num_n_tiles);
+        const uint32_t g = r / per_group;
+        const uint32_t first_m = g * static_cast<uint32_t>(p.group_m);
+        const uint32_t rem_m = static_cast<uint32_t>(p.num_m_tiles) - first_m;
+        const uint32_t gsz = rem_m < static_cast<uint32_t>(p.group_m) ? rem_m : static_cast<uint32_t>(p.group_m);
+        const uint32_t rr = r - g * per_group;
+        const uint32_t q = rr / gsz;
+        b = static_cast<int>(ub);
+        mt = static_cast<int>(first_m + (rr - q * gsz));
+        nt = static_cast<int>(q);
+        return;
+    }
     const long long per_batch = static_cast<long long>(p.num_m_tiles) * p.num_n_tiles;
     b = static_cast<int>(t / per_batch);
     const long long r = t - static_cast<long long>(b) * per_batch;
@@ -243,7 +271,6 @@ __device__ __forceinline__ void decode_tile(const Params& p, long long t, int ti
     const int rr = static_cast<int>(r - static_cast<long long>(g) * per_group);
     mt = first_m + rr % gsz;
     nt = rr / gsz;
-    (void)tile_m;
 }
 
 // Work of one cluster, in the order the producer and MMA process it: data-parallel tiles
@@ -377,6 +404,13 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     const uint32_t IDESC = ptx::make_idesc_f16(C_::kRows * CG, C_::kUmmaN, A_MN, B_MN);
 
     const unsigned long long g_entry = GE_DBG ? globaltimer() : 0ull;
+
+    unsigned long long* tl = nullptr;      // timeline slot of this launch (CTA 0, diagnostics build)
+#if GE_DBG
+#define GE_TL(k, cond) do { if (tl && (cond)) tl[k] = globaltimer(); } while (0)
+#else
+#define GE_TL(k, cond) do { } while (0)
+#endif
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms, by pointer arithmetic on the __shared__ array so
     // the compiler keeps the shared address space (LDS/STS instead of generic LD/ST)
@@ -396,6 +430,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     uint64_t* peer_ready_bar = bars + 3 * S + 6;  // split-K: every peer's ring is free to receive
     uint64_t* recv_full_bar = bars + 3 * S + 7;   // split-K: all partials addressed to this CTA landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 8);
+#if GE_DBG
+    int& tl_slot = reinterpret_cast<int*>(tmem_slot)[1];   // spare word of the barrier area
+    if (threadIdx.x == 0) tl_slot = (p.tl && blockIdx.x == 0) ? static_cast<int>(atomicAdd(p.tl, 1ull)) : -1;
+#endif
     const bool split_cluster = (CG == 1) && p.splits > 1;
 
     const int warp = threadIdx.x / 32;
@@ -438,28 +476,40 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     int pr_wi = 0, pr_kb = 0, pr_s = 0;
     uint32_t pr_phase = 0;
     bool pr_open = false;
+    int pr_issued = 0;                  // k-blocks issued: the first ring pass finds every slot free
+    Piece pr_pc{};                      // the open piece and its decoded tile origin
+    int pr_b = 0, pr_m0 = 0, pr_n0 = 0;
     const uint64_t pol_a = ptx::l2_policy(p.hint_a);
     const uint64_t pol_b = ptx::l2_policy(p.hint_b);
+    // Opening a piece decodes its tile (integer divisions); the first one is opened before the setup
+    // barrier and griddepcontrol.wait, so the first loads issue right after the wait.
+    auto open_piece = [&]() {
+        pr_pc = work.get(pr_wi);
+        pr_kb = pr_pc.kb0;
+        pr_open = true;
+        int mt, nt;
+        decode_tile(p, pr_pc.tile, TILE_M, pr_b, mt, nt);
+        pr_m0 = mt * TILE_M + pair * C_::kTileM + rank * C_::kRows;
+        pr_n0 = nt * BN + rank * C_::kBBlockRows;             // + h * kUmmaN per MMA block
+    };
     auto produce = [&](int budget) {
         int& s = pr_s;
         uint32_t& phase = pr_phase;
         while (pr_wi < work.count() && budget > 0) {
             const int wi = pr_wi;
-            const Piece pc = work.get(wi);
-            if (!pr_open) {
-                pr_kb = pc.kb0;
-                pr_open = true;
-            }
-            const long long t = pc.tile;
-            int b, mt, nt;
-            decode_tile(p, t, TILE_M, b, mt, nt);
-            const int m0 = mt * TILE_M + pair * C_::kTileM + rank * C_::kRows;
-            const int n0 = nt * BN + rank * C_::kBBlockRows;   // + h * kUmmaN per MMA block
+            if (!pr_open) open_piece();
+            const Piece pc = pr_pc;
+            const int b = pr_b, m0 = pr_m0, n0 = pr_n0;
+            GE_TL(TL_P_DECODE, lane == 0 && wi == 0 && pr_kb == pc.kb0);
             for (; pr_kb < pc.kb1 && budget > 0; ++pr_kb, --budget) {
                 const int kb = pr_kb;
+                const bool first_pass = pr_issued < S;
+                ++pr_issued;
                     // paired release: the MMA warp commits only the odd stage of each pair (that
                     // commit covers the even stage's MMAs too), so wait once per pair on it
-                    if (kPairAcq) {
+                    if (first_pass) {
+                        // slots of the first ring pass are free (their barriers' previous-phase parity)
+                    } else if (kPairAcq) {
                         if ((s & 1) == 0) ptx::mbar_wait_timed(&empty_bar[s + 1], phase ^ 1, dbg && lane == 0, dl[DBG_PROD_EMPTY]);
                     } else if (s % kRel == 0) {
                         ptx::mbar_wait_timed(&empty_bar[s + kRel - 1], phase ^ 1, dbg && lane == 0, dl[DBG_PROD_EMPTY]);
@@ -485,6 +535,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         if (++s == S) { s = 0; phase ^= 1; }
                         continue;
                     }
+                    GE_TL(TL_P_EMPTY, lane == 0 && wi == 0 && kb == pc.kb0);
                     auto expect = [&](uint32_t bytes) {
                         if (GE_PROD_WARP) ptx::mbar_arrive_expect_tx_elect(fb, bytes);
                         else ptx::mbar_arrive_expect_tx(fb, bytes);
@@ -521,8 +572,10 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             load(dst, map, k0, m0, pol_a, cb);
                         }
                     };
+                    GE_TL(TL_P_EXPECT, lane == 0 && wi == 0 && kb == pc.kb0);
                     if (do_a) {
                         load_a(sa, map_a, b);
+                        GE_TL(TL_P_LOADA, lane == 0 && wi == 0 && kb == pc.kb0);
                         if constexpr (PRO == 2) load_a(smem_s + s * C_::kSStage, &tmap_p, p.s_batched ? b : 0);
                     }
 #pragma unroll
@@ -545,6 +598,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         }
                     }
                     if (dbg && lane == 0) dl[DBG_PROD_ISSUE] += static_cast<unsigned long long>(clock64() - tp0);
+                    GE_TL(TL_PROD_FIRST, lane == 0 && wi == 0 && kb == pc.kb0);
+                    GE_TL(TL_PROD_LAST, lane == 0);
                     if (kPairAcq && (s & 1) == 0 && !pair_two) ++s;   // single at the end of a piece
                     if (++s == S) { s = 0; phase ^= 1; }
             }
@@ -578,16 +633,25 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         ptx::grid_dependency_wait();                 // inputs may come from the previous kernel
         if (GE_PROD_WARP || lane == 0) produce(S);
     }
+    if ((warp == 0 || (kSplitProd && warp == 3)) && !kEarly && work.count() > 0) open_piece();
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
     ptx::tc_fence_before();
     if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+#if GE_DBG
+    tl = tl_slot >= 0 ? p.tl + 1 + static_cast<long long>(tl_slot) * TL_N : nullptr;
+    if (tl && threadIdx.x == 0) {
+        tl[TL_ENTRY] = g_entry;
+        tl[TL_SETUP] = globaltimer();
+    }
+#endif
     // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
     // prefetch, cluster sync) overlapped the previous kernel's tail; wait for it to complete before
     // touching global memory, then let the next launch in the stream get scheduled.
     ptx::grid_dependency_wait();
     ptx::launch_dependents();
+    GE_TL(TL_WAIT, threadIdx.x == 0);
 
     t_start = clock64();
     if (dbg && warp == 1 && lane == 0) {
@@ -671,6 +735,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                             npend = 0;
                         }
                         wait_ready(s, phase, dl[DBG_MMA_FULL]);
+                        GE_TL(TL_FIRST_FULL, lane == 0 && it == 0 && kb == pc.kb0);
                         ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             ptx::mbar_wait_timed(&tempty_bar[0], acc_phase ^ 1,
@@ -702,6 +767,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         }
                     }
                     ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
+                    GE_TL(TL_LAST_COMMIT, lane == 0);
                 } else if constexpr (kPairAcq) {
                     // paired acquire: one barrier wait and one commit per ring-slot pair
                     for (int kb = pc.kb0; kb < pc.kb1;) {
@@ -724,6 +790,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 } else {
                     for (int kb = pc.kb0; kb < pc.kb1; ++kb) {
                         if (!(GE_EARLY_TEST && next_ready)) wait_ready(s, phase, dl[DBG_MMA_FULL]);
+                        GE_TL(TL_FIRST_FULL, lane == 0 && it == 0 && kb == pc.kb0);
                         if (GE_FENCE_FULL || PRO) ptx::tc_fence_after();
                         if (kb == pc.kb0) {
                             // first k-block of a tile: the epilogue must have drained this buffer
@@ -742,6 +809,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         const long long ti1 = dbg ? clock64() : 0;
                         release_stage(s);                         // smem slot free once these MMAs finish
                         if (kb == pc.kb1 - 1) ptx::mma_commit_elect<CG>(&tfull_bar[acc], pair_mask);
+                        GE_TL(TL_LAST_COMMIT, lane == 0 && kb == pc.kb1 - 1);
                         if (dbg && lane == 0) {
                             dl[DBG_MMA_ISSUE] += static_cast<unsigned long long>(ti1 - ti0);
                             dl[DBG_MMA_COMMIT] += static_cast<unsigned long long>(clock64() - ti1);
@@ -821,6 +889,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 ptx::tc_fence_after();
             };
             if (nkb > 0) wait_acc();
+            GE_TL(TL_EPI_TFULL, e_idx == 0 && lane == 0);
             const long long t_epi0 = (dbg && e_idx == 0) ? clock64() : 0;
             const uint32_t tm_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C_::kBNT;
 
@@ -1310,6 +1379,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             if (GE_END_WAIT_READ) ptx::bulk_wait_read<0>();
             else ptx::bulk_wait<0>();
         }
+        GE_TL(TL_EPI_END, e_idx == 0 && lane == 0);
         if (dbg && e_idx == 0 && lane == 0) {
             dl[DBG_EPI_END] = static_cast<unsigned long long>(clock64() - t_start);
             dl[DBG_G_EPI_END] = globaltimer();
@@ -1441,12 +1511,16 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     }
     ptx::tc_fence_before();
     if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
+    GE_TL(TL_TEARDOWN, threadIdx.x == 0);
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<CG>(tmem_base, C_::kTmemCols);
+        GE_TL(TL_EXIT, lane == 0);
         if (GE_DBG && p.dbg != nullptr && lane == 0) atomicAdd(p.dbg + blockIdx.x * DBG_SLOTS + DBG_G_EXIT, globaltimer());
     }
 #endif
 }
+
+#undef GE_TL
 
 }  // namespace ge

@@ -1,0 +1,6 @@
+#!/bin/bash
+O=gpurun_out/r02s3f
+mkdir -p $O
+export GE_LIBRARY_FILE=$PWD/paper_2006_12645_b200/libgemm_epilogue_dbg.so
+timeout 300 python scripts/timeline.py "256 256 256 rr" "1024 1024 1024 rr" "2048 2048 2048 rr" "35 8464 2560 rr" "5124 704 2048 rr" > $O/timeline.txt 2>&1
+cat $O/timeline.txt
