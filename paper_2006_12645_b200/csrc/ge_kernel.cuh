@@ -94,6 +94,9 @@
 // tcgen05.fence::after_thread_sync after every full-barrier wait of the MMA warp (1), or only after
 // the waits that order TMEM accesses (tile starts, accumulator-empty waits) (0): the TMA bytes a full
 // barrier announces are async-proxy writes the MMA (async proxy) may read once the phase completed.
+#ifndef GE_DBG_NOLOAD_BUILD
+#define GE_DBG_NOLOAD_BUILD 0
+#endif
 #ifndef GE_FENCE_FULL
 #define GE_FENCE_FULL 1
 #endif
@@ -614,6 +617,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     // TMA touches only this CTA's barriers; pairs and multicast clusters signal peer barriers and
     // must wait for the cluster barrier).
     constexpr bool kEarly = GE_EARLY_FILL && CG == 1 && !MC && !kSplitProd;
+    // lean producer loop for every configuration except the dev-flag variants (paired acquire,
+    // split producer, early fill) and the diagnostics build's no-load experiment
+#ifndef GE_LEAN_PROD
+#define GE_LEAN_PROD 1
+#endif
+    constexpr bool kLeanProd = GE_LEAN_PROD && !kPairAcq && !kSplitProd && !kEarly && !GE_DBG_NOLOAD_BUILD;
     if (warp == (kEarly ? 0 : 1) && lane == 0) {
         for (int s = 0; s < S; ++s) {
             // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier and
@@ -658,7 +667,78 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         dl[DBG_G_ENTRY] = g_entry;
         dl[DBG_G_START] = globaltimer();
     }
-    if (warp == 0 || (kSplitProd && warp == 3)) {
+    if (kLeanProd && warp == 0) {
+        // ===================== TMA producer (lean loop) =====================
+        // One thread, every loop variable derived from launch-uniform values so ptxas keeps them in
+        // uniform registers, shared-window addresses precomputed, no elect / cache-hint operands:
+        // the per-k-block issue path was the bound of narrow tiles (DESIGN.md "TMA producer issue
+        // cost": a lean issue loop sustains ~220 B/ns per SM, the general one ~40).
+        if (lane == 0 && work.count() > 0) {
+            const uint32_t a_s0 = ptx::smem_u32(smem_a), b_s0 = ptx::smem_u32(smem_b), x_s0 = ptx::smem_u32(smem_s);
+            const uint32_t fb0 = ptx::smem_u32(full_bar), eb0 = ptx::smem_u32(empty_bar);
+            // every CTA arms its own stage, except CTA pairs without a transform: the leader expects
+            // both CTAs' bytes (the peer's loads signal the leader's barrier)
+            const bool arm = (CG == 1) || (PRO != 0) || leader;
+            const uint32_t bytes = (CG == 2 && !PRO) ? 2u * C_::kStageBytes : static_cast<uint32_t>(C_::kStageBytes);
+            const uint16_t mc_mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
+            int stage = 0, issued = 0;
+            uint32_t ph = 0;
+            for (int wi = 0; wi < work.count(); ++wi) {
+                if (wi > 0 || !pr_open) {
+                    pr_wi = wi;
+                    open_piece();
+                }
+                const int b = pr_b, m0 = pr_m0, n0 = pr_n0;
+                const int kb0 = pr_pc.kb0, kb1 = pr_pc.kb1;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    if (issued >= S && stage % kRel == 0) ptx::mbar_wait_u32(eb0 + 8u * (stage + kRel - 1), ph ^ 1u);
+                    ++issued;
+                    const uint32_t fb = fb0 + 8u * stage;
+                    if (arm) ptx::mbar_expect_tx_u32(fb, bytes);
+                    const bool second = kb >= p.num_k_blocks1;
+                    const CUtensorMap* map_a = second ? &tmap_p : &tmap_a;
+                    const CUtensorMap* map_b = second ? &tmap_q : &tmap_b;
+                    const int k0 = (second ? kb - p.num_k_blocks1 : kb) * kBK;
+                    auto ld = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2) {
+                        if constexpr (CG == 2 && !PRO) ptx::tma_ld3_pair(dst, map, fb, c0, c1, c2);
+                        else ptx::tma_ld3(dst, map, fb, c0, c1, c2);
+                    };
+                    auto ld_a = [&](uint32_t dst, const CUtensorMap* map, int cb) {
+                        if (A_MN) {
+#pragma unroll
+                            for (int i = 0; i < C_::kRows / 64; ++i) ld(dst + i * 8192, map, m0 + i * 64, k0, cb);
+                        } else {
+                            ld(dst, map, k0, m0, cb);
+                        }
+                    };
+                    ld_a(a_s0 + stage * C_::kAStage, map_a, b);
+                    if constexpr (PRO == 2) ld_a(x_s0 + stage * C_::kSStage, &tmap_p, p.s_batched ? b : 0);
+                    const uint32_t sb = b_s0 + stage * C_::kBStage;
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        const uint32_t sbh = sb + h * C_::kBBlockBytes;
+                        const int nh = n0 + h * C_::kUmmaN;
+                        if constexpr (MC) {
+                            const int c0 = B_MN ? nh + pair * 64 : k0, c1 = B_MN ? k0 : nh + pair * 64;
+                            ptx::tma_ld3_pair_mc(sbh + pair * 8192, map_b, fb, c0, c1, b, mc_mask);
+                        } else if (B_MN) {
+#pragma unroll
+                            for (int i = 0; i < C_::kBBlockRows / 64; ++i) ld(sbh + i * 8192, map_b, nh + i * 64, k0, b);
+                        } else {
+                            ld(sbh, map_b, k0, nh, b);
+                        }
+                    }
+                    GE_TL(TL_PROD_FIRST, wi == 0 && kb == kb0);
+                    GE_TL(TL_PROD_LAST, true);
+                    if (++stage == S) {
+                        stage = 0;
+                        ph ^= 1u;
+                    }
+                }
+                pr_open = false;
+            }
+        }
+    } else if (warp == 0 || (kSplitProd && warp == 3)) {
         // ===================== TMA producer =====================
         // GE_PROD_WARP: the whole warp runs the loop converged (warp-uniform state) and one elected
         // lane issues each TMA / expect_tx; otherwise lane 0 alone.  With the early fill the first
