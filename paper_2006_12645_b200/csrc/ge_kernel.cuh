@@ -225,7 +225,9 @@ struct Cfg {
     static constexpr bool kBiasF32 = BN <= 256;
     static constexpr int kBiasBytes = BN * (kBiasF32 ? 4 : 2);
     static constexpr int kStagesRaw = (kSmemBudget - 1024 - kStagingBytes - kBiasBytes - kBarBytes) / kStageBytes;
-    static constexpr int kStages = kStagesRaw > 8 ? 8 : (GE_PAIR_RELEASE ? kStagesRaw & ~1 : kStagesRaw);
+    // paired stage release needs an even ring; a 3-stage ring (the Hadamard prologue's 64 KB stages)
+    // keeps its third stage and releases stage by stage
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : (GE_PAIR_RELEASE && kStagesRaw >= 4 ? kStagesRaw & ~1 : kStagesRaw);
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStagingBytes + kBiasBytes + kBarBytes;
     // fp32 accumulator in TMEM: double-buffered when two fit in the 512 columns, else one buffer
     // drained half by half (per-half barriers let the next tile's first MMAs start early).
@@ -235,7 +237,7 @@ struct Cfg {
     static constexpr int kTmemCols = kTmemUsed <= 32 ? 32 : kTmemUsed <= 64 ? 64 : kTmemUsed <= 128 ? 128
                                    : kTmemUsed <= 256 ? 256 : 512;
     static_assert(kStages >= 2, "not enough smem for a pipeline");
-    static_assert(!GE_PAIR_RELEASE || kStages % 2 == 0, "paired stage release needs an even ring");
+
     static_assert(kBarBytes >= (3 * 8 + 8) * 8 + 4, "barrier area");
     static_assert(kSmemBytes <= kSmemBudget, "smem overflow");
     static_assert(BN == 64 || BN == 128 || BN == 192 || BN == 256 || (BN == 512 && CG == 2), "BN");
@@ -401,8 +403,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     constexpr int EPI_WARPS = epi_warps(OUT_F32, PRO != 0);
     constexpr int NH = C_::kNHalves;
     constexpr int HALF_COLS = BN / NH;
-    constexpr bool kPairAcq = GE_PAIR_ACQ && !PRO && NH == 1 && !MC && GE_PAIR_RELEASE;
-    constexpr int kRel = (GE_PAIR_RELEASE && !kPairAcq) ? ((GE_RELEASE_GROUP == 4 && S % 4 == 0) ? 4 : 2) : 1;
+    constexpr bool kPairAcq = GE_PAIR_ACQ && !PRO && NH == 1 && !MC && GE_PAIR_RELEASE && S % 2 == 0;
+    constexpr int kRel = (GE_PAIR_RELEASE && !kPairAcq && S % 2 == 0) ? ((GE_RELEASE_GROUP == 4 && S % 4 == 0) ? 4 : 2) : 1;
     const bool A_MN = p.a_mn != 0, B_MN = p.b_mn != 0;       // MN-major (row-major B / col-major A)
     const uint32_t IDESC = ptx::make_idesc_f16(C_::kRows * CG, C_::kUmmaN, A_MN, B_MN);
 

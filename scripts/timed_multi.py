@@ -45,6 +45,8 @@ for spec in args:
     bias = torch.randn(N, device="cuda", dtype=torch.float16)
     C = torch.empty(M, ld8(N), device="cuda", dtype=torch.float16)[:, :N]
     scale = (torch.rand(K, device="cuda") + 0.5) if pro == "scale_k" else None
+    if pro == "hadamard":          # the M x K tile S in A's layout
+        scale = operand(M, K, lay[0], 1)[0]
     kw = dict(prologue=pro, scale=scale) if pro else {}
     kw.update(xkw)
     G = 20
