@@ -411,6 +411,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     const unsigned long long g_entry = GE_DBG ? globaltimer() : 0ull;
 
     unsigned long long* tl = nullptr;      // timeline slot of this launch (CTA 0, diagnostics build)
+    (void)tl;
 #if GE_DBG
 #define GE_TL(k, cond) do { if (tl && (cond)) tl[k] = globaltimer(); } while (0)
 #else

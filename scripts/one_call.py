@@ -23,6 +23,8 @@ A = operand(M, K, lay[0])
 B = operand(K, N, lay[1])
 bias = torch.randn(N, device="cuda", dtype=torch.float16)
 scale = torch.rand(K, device="cuda") + 0.5 if pro == "scale_k" else None
+if pro == "hadamard":                  # the M x K tile S in A's layout
+    scale = operand(M, K, lay[0])[0]
 C = torch.empty(batch, M, ld8(N), device="cuda", dtype=torch.float16)[:, :, :N]
 for _ in range(reps):
     if batch == 1:

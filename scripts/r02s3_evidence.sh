@@ -1,0 +1,35 @@
+#!/bin/bash
+# Round-2 evidence on the current build (run from the repo root on a GPU box): GPU tests, the
+# default bench line + per-workload lines, the ncu launch list of the bench command, ncu --set full
+# captures of every bench workload's kernel, paper-shaped sweeps, the tune sweep, compute-sanitizer.
+O=gpurun_out/evidence3
+mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+for w in square256 square1024 square2048 square4096 deepbench_a deepbench_b prologue4096 hadamard4096 batched64x2048; do
+  timeout 300 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu-baseline >> $O/bench_workloads.jsonl 2>> $O/bench_workloads.err
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_square8192.csv \
+  python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-comparators --no-cpu-baseline --no-scale-series > $O/bench_under_ncu.log 2>&1
+cap() {  # workload M N K lay pro batch
+  timeout 600 ncu --set full --import-source on --clock-control none -c 1 -k regex:ge_fused -o $O/$1 \
+    python scripts/one_call.py $2 $3 $4 $5 0 0 2 $6 $7 > $O/$1.log 2>&1
+}
+cap square8192 8192 8192 8192 rr none 1
+cap square4096 4096 4096 4096 rr none 1
+cap square2048 2048 2048 2048 rr none 1
+cap square1024 1024 1024 1024 rr none 1
+cap square256 256 256 256 rr none 1
+cap deepbench_a 5124 700 2048 rr none 1
+cap deepbench_b 35 8457 2560 rr none 1
+cap prologue4096 4096 4096 4096 rr scale_k 1
+cap hadamard4096 4096 4096 4096 rr hadamard 1
+cap batched64x2048 2048 2048 2048 rr none 64
+timeout 1200 python scripts/paper_sweep.py --cpg 20 --out $O/paper_sweep_cpg20.json > $O/paper_sweep_cpg20.log 2>&1
+timeout 1200 python scripts/paper_sweep.py --cpg 1 --out $O/paper_sweep.json > $O/paper_sweep.log 2>&1
+timeout 1200 python scripts/tune_sweep.py > $O/tune_rr_default.log 2>&1; cp gpurun_out/tune_sweep.json $O/tune_rr_default.json
+for t in memcheck synccheck racecheck; do
+  echo "== $t" >> $O/compute_sanitizer.txt
+  timeout 1200 compute-sanitizer --tool $t --print-limit 10 python scripts/sanitize.py >> $O/compute_sanitizer.txt 2>&1
+done
+ls -la $O

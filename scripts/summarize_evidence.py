@@ -18,7 +18,8 @@ prof = os.path.join(ROOT, "profiles")
 shapes = {"square8192": (1, 8192, 8192, 8192, None), "square4096": (1, 4096, 4096, 4096, None),
           "square2048": (1, 2048, 2048, 2048, None), "square256": (1, 256, 256, 256, None),
           "deepbench_a": (1, 5124, 700, 2048, None), "deepbench_b": (1, 35, 8457, 2560, None),
-          "prologue4096": (1, 4096, 4096, 4096, "scale_k"), "batched64x2048": (64, 2048, 2048, 2048, None)}
+          "prologue4096": (1, 4096, 4096, 4096, "scale_k"), "hadamard4096": (1, 4096, 4096, 4096, "hadamard"),
+          "square1024": (1, 1024, 1024, 1024, None), "batched64x2048": (64, 2048, 2048, 2048, None)}
 for w, (b, M, N, K, pro) in shapes.items():
     rep = os.path.join(d, w + ".ncu-rep")
     if not os.path.exists(rep):
@@ -38,6 +39,8 @@ for src, dst in (("bench_default.json", f"{tag}_bench_square8192.json"),
                  ("bench_workloads.jsonl", f"{tag}_bench_workloads.jsonl"),
                  ("paper_sweep.json", f"{tag}_paper_sweep.json"),
                  ("paper_sweep_cpg20.json", f"{tag}_paper_sweep_cpg20.json"),
-                 ("pytest_gpu.log", f"{tag}_pytest_gpu.log")):
+                 ("pytest_gpu.log", f"{tag}_pytest_gpu.log"),
+                 ("tune_rr_default.json", f"{tag}_tune_rr_default.json"),
+                 ("compute_sanitizer.txt", f"{tag}_compute_sanitizer.txt")):
     if os.path.exists(os.path.join(d, src)):
         shutil.copy(os.path.join(d, src), os.path.join(prof, dst))
