@@ -2,8 +2,11 @@
 # Round-2 evidence on the current build (run from the repo root on a GPU box): GPU tests, the
 # default bench line + per-workload lines, the ncu launch list of the bench command, ncu --set full
 # captures of every bench workload's kernel, paper-shaped sweeps, the tune sweep, compute-sanitizer.
-O=gpurun_out/evidence3
-mkdir -p $O
+O=/tmp/ev3
+G=gpurun_out/evidence3
+rm -rf $O; mkdir -p $O $G $G/profiles
+exec > >(tee $G/steps.log) 2>&1
+set -x
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
 for w in square256 square1024 square2048 square4096 deepbench_a deepbench_b prologue4096 hadamard4096 batched64x2048; do
@@ -33,3 +36,8 @@ for t in memcheck synccheck racecheck; do
   timeout 1200 compute-sanitizer --tool $t --print-limit 10 python scripts/sanitize.py >> $O/compute_sanitizer.txt 2>&1
 done
 ls -la $O
+python scripts/summarize_evidence.py $O 2 > $G/summarize.log 2>&1
+cp profiles/r02_* profiles/ncu_summary.json $G/profiles/ 2>/dev/null
+cp $O/*.json $O/*.jsonl $O/*.log $O/*.txt $O/*.err $O/*.csv $G/ 2>/dev/null
+for f in $O/*.ncu-rep; do ncu -i $f --page raw --csv > $G/$(basename $f .ncu-rep)_raw.csv 2>/dev/null; done
+du -sh $G
