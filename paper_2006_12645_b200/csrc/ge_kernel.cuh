@@ -94,6 +94,10 @@
 // tcgen05.fence::after_thread_sync after every full-barrier wait of the MMA warp (1), or only after
 // the waits that order TMEM accesses (tile starts, accumulator-empty waits) (0): the TMA bytes a full
 // barrier announces are async-proxy writes the MMA (async proxy) may read once the phase completed.
+// Teardown cluster barrier without the release fence (execution sync only; see cluster_sync_relaxed).
+#ifndef GE_TEARDOWN_RELAXED
+#define GE_TEARDOWN_RELAXED 1
+#endif
 #ifndef GE_DBG_NOLOAD_BUILD
 #define GE_DBG_NOLOAD_BUILD 0
 #endif
@@ -1593,7 +1597,12 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
             if (dl[i]) atomicAdd(dg + i, dl[i]);
     }
     ptx::tc_fence_before();
-    if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
+    if (CG == 2 || split_cluster) {
+        if (GE_TEARDOWN_RELAXED) ptx::cluster_sync_relaxed();
+        else ptx::cluster_sync();
+    } else {
+        __syncthreads();
+    }
     GE_TL(TL_TEARDOWN, threadIdx.x == 0);
     if (warp == 2) {
         ptx::tc_fence_after();

@@ -181,6 +181,14 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
+// Execution-only cluster barrier for the teardown: every cross-CTA data hand-off of the kernel
+// (TMA bytes, DSMEM partials, MMA completion) is already ordered by an mbarrier the consumer waited
+// on, so exiting only needs "every CTA of the cluster is past its last wait" -- no release fence
+// over this thread's prior writes (which a .release arrive waits for).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
