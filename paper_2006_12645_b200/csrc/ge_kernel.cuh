@@ -309,11 +309,20 @@ struct WorkSeq {
         }
         dp_tiles = p.dp_tiles;
         units = p.sk_units;
-        n_dp = dp_tiles > cid ? static_cast<int>((dp_tiles - cid + G - 1) / G) : 0;
-        u0 = range_begin(cid);
-        u1 = range_begin(cid + 1);
+        // 32-bit division where the tile count allows it (64-bit division is a long subroutine and
+        // this runs ahead of the setup barrier)
+        if (dp_tiles <= cid) n_dp = 0;
+        else if (dp_tiles <= 0x7fffffffll)
+            n_dp = static_cast<int>((static_cast<uint32_t>(dp_tiles - cid) + static_cast<uint32_t>(G) - 1u) / static_cast<uint32_t>(G));
+        else
+            n_dp = static_cast<int>((dp_tiles - cid + G - 1) / G);
         n_sk = 0;
-        if (u1 > u0) n_sk = (u1 > (u0 / nkb + 1) * nkb) ? 2 : 1;
+        u0 = u1 = 0;
+        if (units > 0) {                    // stream-K launches only
+            u0 = range_begin(cid);
+            u1 = range_begin(cid + 1);
+            if (u1 > u0) n_sk = (u1 > (u0 / nkb + 1) * nkb) ? 2 : 1;
+        }
     }
     __device__ __forceinline__ long long range_begin(int c) const { return units * c / G; }
     __device__ __forceinline__ int count() const { return n_dp + n_sk; }
@@ -630,18 +639,24 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
 #define GE_LEAN_PROD 1
 #endif
     constexpr bool kLeanProd = GE_LEAN_PROD && !kPairAcq && !kSplitProd && !kEarly && !GE_DBG_NOLOAD_BUILD;
-    if (warp == (kEarly ? 0 : 1) && lane == 0) {
-        for (int s = 0; s < S; ++s) {
+    if (warp == (kEarly ? 0 : 1)) {
+        // one barrier per lane (the ring has at most 8 stages: 3 x 8 + 8 <= 32 barriers)
+        static_assert(3 * S + 8 <= 32, "barrier init: one per lane");
+        if (lane < S) {
             // pair mode without a transform: both CTAs' TMA bytes land on the leader's barrier and
             // only the leader's producer arrives (expecting both CTAs' bytes).
-            ptx::mbar_init(&full_bar[s], 1);
-            ptx::mbar_init(&empty_bar[s], MC ? 2 : 1);      // MC: both pairs' MMAs read stage s's B
-            ptx::mbar_init(&xform_bar[s], kXformWarps * CG);
+            ptx::mbar_init(&full_bar[lane], 1);
+            ptx::mbar_init(&empty_bar[lane], MC ? 2 : 1);   // MC: both pairs' MMAs read stage s's B
+            ptx::mbar_init(&xform_bar[lane], kXformWarps * CG);
+        } else if (lane < S + 2) {
+            ptx::mbar_init(&tfull_bar[lane - S], 1);
+        } else if (lane < S + 6) {
+            ptx::mbar_init(&tempty_bar[lane - S - 2], EPI_WARPS * CG);
+        } else if (lane == S + 6) {
+            ptx::mbar_init(peer_ready_bar, split_cluster ? p.splits - 1 : 1);
+        } else if (lane == S + 7) {
+            ptx::mbar_init(recv_full_bar, 1);
         }
-        for (int b = 0; b < 2; ++b) ptx::mbar_init(&tfull_bar[b], 1);
-        for (int b = 0; b < 4; ++b) ptx::mbar_init(&tempty_bar[b], EPI_WARPS * CG);
-        ptx::mbar_init(peer_ready_bar, split_cluster ? p.splits - 1 : 1);
-        ptx::mbar_init(recv_full_bar, 1);
         ptx::fence_mbar_init();
     }
     if (kEarly && warp == 0) {
