@@ -98,6 +98,10 @@
 #ifndef GE_TEARDOWN_RELAXED
 #define GE_TEARDOWN_RELAXED 1
 #endif
+// griddepcontrol.launch_dependents ahead of griddepcontrol.wait (off the critical path)
+#ifndef GE_EARLY_TRIGGER
+#define GE_EARLY_TRIGGER 1
+#endif
 #ifndef GE_DBG_NOLOAD_BUILD
 #define GE_DBG_NOLOAD_BUILD 0
 #endif
@@ -680,8 +684,15 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
     // prefetch, cluster sync) overlapped the previous kernel's tail; wait for it to complete before
     // touching global memory, then let the next launch in the stream get scheduled.
+#if GE_EARLY_TRIGGER
+    // let the next launch in the stream get scheduled before waiting on the previous one: its CTAs
+    // still wait (griddepcontrol.wait) for this grid's completion before touching memory
+    ptx::launch_dependents();
+    ptx::grid_dependency_wait();
+#else
     ptx::grid_dependency_wait();
     ptx::launch_dependents();
+#endif
     GE_TL(TL_WAIT, threadIdx.x == 0);
 
     t_start = clock64();

@@ -4,7 +4,7 @@
 O=gpurun_out/r02s3g
 mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q -x > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
-GE_LIBRARY_FILE=$PWD/paper_2006_12645_b200/libgemm_epilogue_dbg.so timeout 300 python scripts/timeline.py "256 256 256 rr" "1024 1024 1024 rr" "35 8464 2560 rr" > $O/timeline.txt 2>&1
+GE_LIBRARY_FILE=$PWD/paper_2006_12645_b200/libgemm_epilogue_dbg.so timeout 300 python scripts/timeline.py "256 256 256 rr" "1024 1024 1024 rr" "2048 2048 2048 rr" "35 8464 2560 rr" "5124 704 2048 rr" > $O/timeline.txt 2>&1
 SH=("256 256 256 rr" "1024 1024 1024 rr" "2048 2048 2048 rr" "5124 704 2048 rr" "35 8464 2560 rr" "640 1024 3840 rc" "1536 1280 2432 rc" "4096 4096 4096 rr" "8192 8192 8192 rr")
 for rep in 1 2; do
 for v in trans default; do
