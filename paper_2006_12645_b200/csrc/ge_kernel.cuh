@@ -102,6 +102,10 @@
 #ifndef GE_EARLY_TRIGGER
 #define GE_EARLY_TRIGGER 1
 #endif
+// the lean producer's griddepcontrol.wait sits right before its first TMA load
+#ifndef GE_PROD_LATE_WAIT
+#define GE_PROD_LATE_WAIT 1
+#endif
 #ifndef GE_DBG_NOLOAD_BUILD
 #define GE_DBG_NOLOAD_BUILD 0
 #endif
@@ -181,7 +185,9 @@ struct Params {
 enum : int { TL_ENTRY = 0, TL_SETUP = 1, TL_WAIT = 2, TL_FIRST_FULL = 3, TL_LAST_COMMIT = 4, TL_EPI_TFULL = 5,
              TL_EPI_END = 6, TL_TEARDOWN = 7, TL_EXIT = 8, TL_PROD_FIRST = 9, TL_PROD_LAST = 10,
              // producer's first k-block: tile decoded, empty slot acquired, expect_tx armed, A loads issued
-             TL_P_DECODE = 11, TL_P_EMPTY = 12, TL_P_EXPECT = 13, TL_P_LOADA = 14, TL_N = 16 };
+             TL_P_DECODE = 11, TL_P_EMPTY = 12, TL_P_EXPECT = 13, TL_P_LOADA = 14, TL_N = 16,
+             // setup phases (same slots as unused producer stamps of the lean loop)
+             TL_S_BARINIT = 12, TL_S_ALLOC = 15 };
 
 // Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
 enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
@@ -670,6 +676,8 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     }
     if ((warp == 0 || (kSplitProd && warp == 3)) && !kEarly && work.count() > 0) open_piece();
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
+    // setup-phase stamps (diagnostics build), written once the launch's timeline slot is known
+    const unsigned long long t_setup_phase = (GE_DBG && (warp == 1 || warp == 2)) ? globaltimer() : 0ull;
     ptx::tc_fence_before();
     if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
@@ -680,15 +688,19 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         tl[TL_ENTRY] = g_entry;
         tl[TL_SETUP] = globaltimer();
     }
+    if (tl && lane == 0 && warp == 1) tl[TL_S_BARINIT] = t_setup_phase;
+    if (tl && lane == 0 && warp == 2) tl[TL_S_ALLOC] = t_setup_phase;
 #endif
     // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor
     // prefetch, cluster sync) overlapped the previous kernel's tail; wait for it to complete before
     // touching global memory, then let the next launch in the stream get scheduled.
 #if GE_EARLY_TRIGGER
     // let the next launch in the stream get scheduled before waiting on the previous one: its CTAs
-    // still wait (griddepcontrol.wait) for this grid's completion before touching memory
+    // still wait (griddepcontrol.wait) for this grid's completion before touching memory.  The
+    // lean producer waits by itself right before its first load (below), so the code ahead of that
+    // load -- and its instruction-cache misses -- runs while the previous grid finishes.
     ptx::launch_dependents();
-    ptx::grid_dependency_wait();
+    if (!(kLeanProd && GE_PROD_LATE_WAIT && warp == 0)) ptx::grid_dependency_wait();
 #else
     ptx::grid_dependency_wait();
     ptx::launch_dependents();
@@ -724,14 +736,17 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                 const int b = pr_b, m0 = pr_m0, n0 = pr_n0;
                 const int kb0 = pr_pc.kb0, kb1 = pr_pc.kb1;
                 for (int kb = kb0; kb < kb1; ++kb) {
+                    GE_TL(TL_P_DECODE, wi == 0 && kb == kb0);
                     if (issued >= S && stage % kRel == 0) ptx::mbar_wait_u32(eb0 + 8u * (stage + kRel - 1), ph ^ 1u);
                     ++issued;
                     const uint32_t fb = fb0 + 8u * stage;
                     if (arm) ptx::mbar_expect_tx_u32(fb, bytes);
+                    GE_TL(TL_P_EXPECT, wi == 0 && kb == kb0);
                     const bool second = kb >= p.num_k_blocks1;
                     const CUtensorMap* map_a = second ? &tmap_p : &tmap_a;
                     const CUtensorMap* map_b = second ? &tmap_q : &tmap_b;
                     const int k0 = (second ? kb - p.num_k_blocks1 : kb) * kBK;
+                    if (GE_EARLY_TRIGGER && GE_PROD_LATE_WAIT && issued == 1) ptx::grid_dependency_wait();
                     auto ld = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2) {
                         if constexpr (CG == 2 && !PRO) ptx::tma_ld3_pair(dst, map, fb, c0, c1, c2);
                         else ptx::tma_ld3(dst, map, fb, c0, c1, c2);
@@ -745,6 +760,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
                         }
                     };
                     ld_a(a_s0 + stage * C_::kAStage, map_a, b);
+                    GE_TL(TL_P_LOADA, wi == 0 && kb == kb0);
                     if constexpr (PRO == 2) ld_a(x_s0 + stage * C_::kSStage, &tmap_p, p.s_batched ? b : 0);
                     const uint32_t sb = b_s0 + stage * C_::kBStage;
 #pragma unroll

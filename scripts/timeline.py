@@ -54,13 +54,13 @@ for spec in specs:
     print(f"== {spec} {extra}  plan {pl['tile_m']}x{pl['tile_n']} cg{pl['cta_group']} split{pl['split_k']} "
           f"swap{pl['swap_ab']}  launches {n}")
     print("  (ns, relative to this launch's entry; gap = entry - previous exit)")
-    print("   i    gap  setup   wait  pfirst  full1  lastc  tfull  eend  tdown  exit  plast decode  empty expect  loadA")
+    print("   i    gap  setup   wait  pfirst  full1  lastc  tfull  eend  tdown  exit  plast decode barini expect  loadA  alloc")
     rows = []
     for i in range(n):
         r = t[i]
         e = r[0]
         gap = e - t[i - 1][8] if i > 0 else 0
-        rel = [r[k] - e if r[k] else -1 for k in (1, 2, 9, 3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14)]
+        rel = [r[k] - e if r[k] else -1 for k in (1, 2, 9, 3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 15)]
         rows.append([gap] + rel)
         print(f"  {i:2d} {gap:6d} " + " ".join(f"{x:6d}" for x in rel))
     import statistics
