@@ -678,6 +678,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     if (warp == 2) ptx::tmem_alloc<CG>(tmem_slot, C_::kTmemCols);
     // setup-phase stamps (diagnostics build), written once the launch's timeline slot is known
     const unsigned long long t_setup_phase = (GE_DBG && (warp == 1 || warp == 2)) ? globaltimer() : 0ull;
+    (void)t_setup_phase;
     ptx::tc_fence_before();
     if (CG == 2 || split_cluster) ptx::cluster_sync(); else __syncthreads();
     ptx::tc_fence_after();
