@@ -181,6 +181,26 @@ def test_prologue(prologue, layouts, tile_n, cg):
             check_bound(got, out, mag, f"{prologue} {layouts}")
 
 
+@pytest.mark.parametrize("prologue", ["scale_k", "relu"])
+@pytest.mark.parametrize("layouts", ["rr", "cc"])
+def test_prologue_multi_tile(prologue, layouts):
+    """The in-place prologue transform over several tiles per CTA pair (100 tiles of 256 x 256 on at
+    most 74 pairs) and 16 k-blocks, so every ring slot is transformed many times across tiles:
+    bitwise equal to the 256 x 512 tile's launch on small integers (exact in any order), fp16 and
+    fp32 out, and within the bound of the oracle on a sample of rows/columns of uniform data."""
+    M, N, K = 2560, 2560, 1024
+    prob = workloads.make_problem(M, N, K, seed=77, kind="smallint", bias_mode="row", prologue=prologue)
+    for dt in (torch.float16, torch.float32):
+        ta = run_gpu(prob, layouts, tile_n=256, cta_group=2, out_dtype=dt)
+        ref = run_gpu(prob, layouts, tile_n=512, cta_group=2, out_dtype=dt)
+        assert np.array_equal(ta, ref), (prologue, layouts, dt)
+    prob = workloads.make_problem(M, N, K, seed=78, kind="uniform", bias_mode="row", prologue=prologue)
+    got = run_gpu(prob, layouts, tile_n=256, cta_group=2)
+    rows, cols = np.array([0, 127, 128, 255, 256, 1300, M - 1]), np.array([0, 63, 64, 127, 128, 255, 256, 1111, N - 1])
+    out, mag = oracle_run(prob, layouts, rows=rows, cols=cols)
+    check_bound(got[np.ix_(rows, cols)], out, mag, f"multi-tile {prologue} {layouts}")
+
+
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (8, 8, 8), (1, 300, 64), (300, 1, 64), (127, 129, 63), (128, 256, 64),
                                    (129, 257, 65), (64, 64, 4096), (1000, 72, 17)])
 def test_odd_shapes(M, N, K):
