@@ -512,7 +512,7 @@ def run_ours(args):
         if scale_series:
             line["scale_series"] = scale_series
         if not args.no_cpu_baseline:
-            rate, cores, desc, _ = oracle_rate(M, N, K, seed=7, budget_s=12.0, max_side=4096)
+            rate, cores, desc, _ = oracle_rate(M, N, K, seed=7, budget_s=36.0, max_side=4096)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
         print(json.dumps(line), flush=True)
     if world > 1:
