@@ -890,3 +890,32 @@ def test_half_row_pairs_variants(variant):
         got = run_gpu(prob, "rr", op="literal_bias_relu", **kw)
         lit, _ = oracle_run(prob, "rr", literal_round=True)
         assert np.array_equal(got, exact_expect(lit, torch.float16))
+
+
+# ------------------------------------------------------------------ randomized sweep (planner choices)
+@pytest.mark.parametrize("chunk", range(8))
+def test_random_shapes_bitwise(chunk):
+    """A seeded random sweep over shapes (M, N, K in 1..1100 with bias on tile edges, skinny M for
+    swap-AB, long K for split-K), the four layouts, bias modes, out dtypes, prologues and ops,
+    launched with the DEFAULT plan (whatever tile / split-K / swap-AB / stream-K the planner
+    picks): small-integer data is exact in any summation order, so every element must equal
+    RNE(oracle) bitwise (fp32 out: the oracle itself)."""
+    rng = np.random.default_rng(2026 + chunk)
+    for case in range(16):
+        kind_shape = rng.integers(0, 4)
+        if kind_shape == 0:      # skinny M against a long N (swap-AB territory)
+            M, N, K = int(rng.integers(1, 65)), int(rng.integers(1024, 2100)), int(rng.integers(64, 700))
+        elif kind_shape == 1:    # few long tiles (split-K territory)
+            M, N, K = int(rng.integers(64, 700)), int(rng.integers(64, 300)), int(rng.integers(1500, 4000))
+        else:
+            M, N, K = (int(x) for x in rng.integers(1, 1100, size=3))
+        layouts = str(rng.choice(workloads.LAYOUTS))
+        bias_mode = str(rng.choice(["row", "col", "full", "none"]))
+        out_dtype = torch.float32 if rng.random() < 0.3 else torch.float16
+        prologue = str(rng.choice(["none", "none", "scale_k", "relu"])) if bias_mode != "none" else "none"
+        prob = workloads.make_problem(M, N, K, seed=3000 + 100 * chunk + case, kind="smallint",
+                                      bias_mode=bias_mode, prologue=None if prologue == "none" else prologue)
+        what = (M, N, K, layouts, bias_mode, str(out_dtype), prologue)
+        got = run_gpu(prob, layouts, out_dtype=out_dtype, op=None if bias_mode != "none" else "relu")
+        out, _ = oracle_run(prob, layouts)
+        assert np.array_equal(got, exact_expect(out, out_dtype)), what
