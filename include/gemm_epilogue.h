@@ -37,6 +37,9 @@
  * aligned and lda*2, ldb*2 (and batch strides *2) multiples of 16 bytes, else
  * GE_ERR_MISALIGNED.  C, bias and scale have no alignment requirement: a C whose base or
  * ldc is not 16-byte compatible is written by a st.global epilogue instead of TMA stores.
+ * Only the M x N window of C is written: elements past column N-1 of a row (the padding of
+ * ldc > N) keep their contents, also when N*sizeof(C) is not a multiple of 16 bytes (the TMA
+ * store covers the 16-byte-aligned part of each row, the ragged edge is stored element-wise).
  * Aliasing: C must not overlap A, B, bias, scale or the prologue tile (`__restrict__`), else
  * GE_ERR_ALIASING.
  * Degenerate sizes: M == 0 or N == 0 (or batch == 0) is a no-op returning GE_OK.
