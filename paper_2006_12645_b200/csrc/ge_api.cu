@@ -1231,7 +1231,7 @@ int32_t ge_debug_read(uint64_t* out, int32_t max_ctas) {
 }
 
 // Debug build only (not in the header): set the timeline buffer (nullptr: off).  Layout: word 0 =
-// launch counter, then 16 words per launch (see ge_kernel.cuh TL_*).
+// launch counter, then 24 words per launch (see ge_kernel.cuh TL_*).
 void ge_debug_set_timeline(unsigned long long* dev_buf) { g_timeline = dev_buf; }
 
 const char* ge_version(void) { return "gemm_epilogue-b200 0.1.0 (sm_100a, tcgen05/TMA/TMEM)"; }

@@ -185,9 +185,11 @@ struct Params {
 enum : int { TL_ENTRY = 0, TL_SETUP = 1, TL_WAIT = 2, TL_FIRST_FULL = 3, TL_LAST_COMMIT = 4, TL_EPI_TFULL = 5,
              TL_EPI_END = 6, TL_TEARDOWN = 7, TL_EXIT = 8, TL_PROD_FIRST = 9, TL_PROD_LAST = 10,
              // producer's first k-block: tile decoded, empty slot acquired, expect_tx armed, A loads issued
-             TL_P_DECODE = 11, TL_P_EMPTY = 12, TL_P_EXPECT = 13, TL_P_LOADA = 14, TL_N = 16,
+             TL_P_DECODE = 11, TL_P_EMPTY = 12, TL_P_EXPECT = 13, TL_P_LOADA = 14, TL_N = 24,
              // setup phases (same slots as unused producer stamps of the lean loop)
-             TL_S_BARINIT = 12, TL_S_ALLOC = 15 };
+             TL_S_BARINIT = 12, TL_S_ALLOC = 15,
+             // MMA warp lane 0: after the work sequence is built, after the L2 policies
+             TL_S_WORKSEQ = 16, TL_S_POLICY = 17 };
 
 // Diagnostics slots per CTA (cycles blocked on each barrier; see ge_debug_read in the header).
 enum : int { DBG_TOTAL = 0, DBG_PROD_EMPTY = 1, DBG_MMA_FULL = 2, DBG_MMA_TEMPTY = 3, DBG_EPI_TFULL = 4,
@@ -491,6 +493,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     const int num_clusters = gridDim.x / CL;
     const int nkb = p.num_k_blocks;
     const WorkSeq work(p, cluster_id, num_clusters);
+    const unsigned long long t_ws = GE_DBG ? globaltimer() : 0ull;
     // Diagnostics accumulate in registers (a global read-modify-write per barrier wait would add
     // an L2 round trip to every pipeline step) and are flushed once per thread at teardown.
     const bool dbg = GE_DBG && p.dbg != nullptr;
@@ -509,6 +512,7 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
     Piece pr_pc{};                      // the open piece and its decoded tile origin
     int pr_b = 0, pr_m0 = 0, pr_n0 = 0;
     const uint64_t pol_a = ptx::l2_policy(p.hint_a);
+    const unsigned long long t_pol = GE_DBG ? globaltimer() : 0ull;
     const uint64_t pol_b = ptx::l2_policy(p.hint_b);
     // Opening a piece decodes its tile (integer divisions); the first one is opened before the setup
     // barrier and griddepcontrol.wait, so the first loads issue right after the wait.
@@ -689,7 +693,11 @@ ge_fused_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constan
         tl[TL_ENTRY] = g_entry;
         tl[TL_SETUP] = globaltimer();
     }
-    if (tl && lane == 0 && warp == 1) tl[TL_S_BARINIT] = t_setup_phase;
+    if (tl && lane == 0 && warp == 1) {
+        tl[TL_S_BARINIT] = t_setup_phase;
+        tl[TL_S_WORKSEQ] = t_ws;
+        tl[TL_S_POLICY] = t_pol;
+    }
     if (tl && lane == 0 && warp == 2) tl[TL_S_ALLOC] = t_setup_phase;
 #endif
     // Programmatic dependent launch: everything above (barrier init, TMEM allocation, descriptor

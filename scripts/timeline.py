@@ -33,7 +33,7 @@ for spec in specs:
     bias = torch.randn(N, device="cuda", dtype=torch.float16)
     C = torch.empty(M, ld8(N), device="cuda", dtype=torch.float16)[:, :N]
     G = 20
-    buf = torch.zeros(1 + 16 * 64, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(1 + 24 * 64, dtype=torch.int64, device="cuda")
     lib.ge_debug_set_timeline(ctypes.c_void_p(buf.data_ptr()))
     call = lambda i: ge.gemm_epilogue(As[i % nset], Bs[i % nset], bias, out=C, tile_n=bn, cta_group=cg, **xkw)
     for i in range(3):
@@ -49,18 +49,18 @@ for spec in specs:
     torch.cuda.synchronize()
     lib.ge_debug_set_timeline(ctypes.c_void_p(0))
     n = int(buf[0].item())
-    t = buf[1:1 + 16 * n].view(n, 16).cpu().tolist()
+    t = buf[1:1 + 24 * n].view(n, 24).cpu().tolist()
     pl = ge.plan(M, N, K, layouts=lay, tile_n=bn, cta_group=cg, **xkw)
     print(f"== {spec} {extra}  plan {pl['tile_m']}x{pl['tile_n']} cg{pl['cta_group']} split{pl['split_k']} "
           f"swap{pl['swap_ab']}  launches {n}")
     print("  (ns, relative to this launch's entry; gap = entry - previous exit)")
-    print("   i    gap  setup   wait  pfirst  full1  lastc  tfull  eend  tdown  exit  plast decode barini expect  loadA  alloc")
+    print("   i    gap  setup   wait  pfirst  full1  lastc  tfull  eend  tdown  exit  plast decode barini expect  loadA  alloc  wseq policy")
     rows = []
     for i in range(n):
         r = t[i]
         e = r[0]
         gap = e - t[i - 1][8] if i > 0 else 0
-        rel = [r[k] - e if r[k] else -1 for k in (1, 2, 9, 3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 15)]
+        rel = [r[k] - e if r[k] else -1 for k in (1, 2, 9, 3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 15, 16, 17)]
         rows.append([gap] + rel)
         print(f"  {i:2d} {gap:6d} " + " ".join(f"{x:6d}" for x in rel))
     import statistics
