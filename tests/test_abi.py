@@ -195,6 +195,22 @@ def test_no_device_fails_loudly(ge):
         ge.gemm_epilogue(A, A)
 
 
+def test_missing_library_fails_loudly(tmp_path):
+    """Without the compiled CUDA library the package raises on first use (ImportError naming the
+    build command); there is no CPU fallback path to take instead."""
+    import subprocess
+    import sys
+    code = ("import torch, paper_2006_12645_b200 as ge\n"
+            "try:\n"
+            "    ge.gemm_epilogue(torch.zeros((8, 8), dtype=torch.float16), torch.zeros((8, 8), dtype=torch.float16))\n"
+            "except ImportError as e:\n"
+            "    print('IMPORTERROR', e)\n")
+    env = dict(os.environ, GE_LIBRARY_FILE=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+    assert "IMPORTERROR" in r.stdout and "build" in r.stdout, (r.stdout, r.stderr[-500:])
+
+
 def test_binding_layout_detection(ge):
     X = torch.zeros((96, 40), dtype=torch.float16)
     assert ge.layout_of(X) == (0, 40)
